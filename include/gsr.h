@@ -1,0 +1,190 @@
+/*
+ * gsr.h -- C ABI of libgsr, the B200-native (sm_100a) active-view scoring
+ * rasterizer for DAV-GSWT (arXiv 2602.15355).
+ *
+ * The paper's problem statement (§3.1): candidate camera poses
+ * Θ_cand = {θ_j} on a hemisphere, θ = (elevation, azimuth, radius); a scalar
+ * uncertainty u(θ) ranks the candidates (§3.2) and the top-k are acquired
+ * (Alg. 1).  The north_star (BASELINE.json) makes u(θ) the mean of the
+ * per-pixel composited per-Gaussian uncertainty, rendered by tile-based 3DGS
+ * forward rasterization (the splat/sort/render pipeline the paper times,
+ * PAPER.md L189 and §3.5).  Every numeric rule below is one of the
+ * readings listed in DESIGN.md "Readings of the paper".
+ *
+ * Conventions
+ *  - Plain C: no C++ types, no exceptions, no torch types.  Pointers are
+ *    DEVICE pointers unless marked [host].  `stream` is a cudaStream_t passed
+ *    as void* (NULL = legacy default stream).
+ *  - Calls enqueue work on `stream` and return without synchronising unless
+ *    marked SYNC.  Outputs are valid once the stream has synchronised.
+ *  - Ownership: the caller allocates every input and output; a gsr_ctx owns
+ *    only scratch (grown on demand, freed by gsr_destroy).  No pointer is
+ *    retained after a call returns.  One context per stream / host thread.
+ *  - Errors: every entry point returns a gsr_status; gsr_last_error(ctx)
+ *    gives the message of the last non-OK status of that context.  Inputs
+ *    must be finite (NaN/Inf is a documented precondition, not checked).
+ *    Culled or off-screen Gaussians are not errors (n_tiles = 0).
+ */
+#ifndef GSR_H
+#define GSR_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct gsr_ctx gsr_ctx;
+
+typedef enum {
+  GSR_OK = 0,
+  GSR_EINVAL = 1,    /* bad argument: NULL required pointer, n < 0, sh_degree not in [0,3],
+                        W/H <= 0, znear <= 0, n_views <= 0 or > GSR_MAX_VIEWS, mixed
+                        resolutions in a batch, V*tiles >= 2^32 */
+  GSR_ECUDA = 2,     /* a CUDA launch or runtime call failed */
+  GSR_ENOMEM = 3,    /* scratch allocation failed */
+  GSR_ECAPACITY = 4, /* key capacity too small: *n_keys holds the required size and
+                        nothing else was written */
+  GSR_EBUDGET = 5    /* k < 1 or k > n - #excluded ("budget error") */
+} gsr_status;
+
+/* Largest number of views in one batch (cameras travel as kernel parameters). */
+#define GSR_MAX_VIEWS 64
+/* Screen tile edge in pixels (BASELINE.json configs[0] "16x16 tiles"). */
+#define GSR_TILE 16
+
+/* The Gaussian field 𝒢 ("Gaussian field", per-Gaussian
+   uncertainty of the north_star).  Planar float4 planes, each n elements,
+   16-byte aligned, device memory:
+     pos_opacity [n][4] = (x, y, z, opacity in (0,1])   opacity already activated
+     scale_unc   [n][4] = (sx, sy, sz > 0, uncertainty >= 0)   std-devs, activated
+     rot         [n][4] = (w, x, y, z)   any non-zero quaternion; normalised in K1
+     sh          [P][n][4], P = ceil(3 (d+1)^2 / 4): plane j, element i holds flat
+                 coefficients 4j..4j+3 of Gaussian i, flat index = 3*coef + channel;
+                 coefficient 0 is the base RGB (DC = colour, no C0 scale/offset). */
+typedef struct {
+  int64_t n;
+  int32_t sh_degree; /* 0..3 */
+  int32_t reserved;
+  const float* pos_opacity;
+  const float* scale_unc;
+  const float* rot;
+  const float* sh;
+} gsr_gaussians;
+
+/* One pinhole camera, world->camera, OpenCV axes (x right, y down, z forward).
+   Built on the host in double and rounded once (gsr_camera_look_at).
+   limx = 1.3 (W/2)/fx and limy = 1.3 (H/2)/fy are the EWA FOV clamp. 96 bytes. */
+typedef struct {
+  float R[9]; /* row-major */
+  float t[3];
+  float campos[3];
+  float fx, fy, cx, cy, limx, limy, znear;
+  int32_t width, height;
+} gsr_camera;
+
+/* ---- context ------------------------------------------------------------ */
+gsr_status gsr_create(gsr_ctx** out, int device);
+gsr_status gsr_destroy(gsr_ctx* ctx);
+/* Message for the last non-OK status of ctx (ctx may be NULL: thread-global). */
+const char* gsr_last_error(const gsr_ctx* ctx);
+/* Library version string, e.g. "gsr 0.1 sm_100a". */
+const char* gsr_version(void);
+
+/* ---- H1 camera builder (host only) --------------------------------------
+   θ = (elevation, azimuth, radius) of PAPER.md L57, looking at `target`
+   [host, 3 doubles]:  eye = target + radius (cos e cos a, sin e, cos e sin a);
+   f = normalize(target - eye); r = normalize(f x up) with up = +y (or +z if
+   |f.y| > 0.9999); d = f x r; R rows (r, d, f); t = -R eye; principal point
+   (W/2, H/2); fx = fy = focal.  Computed in double, rounded once.  EINVAL on
+   W/H <= 0, focal <= 0, znear <= 0, radius <= 0. */
+gsr_status gsr_camera_look_at(double elevation, double azimuth, double radius, const double* target,
+                              int32_t width, int32_t height, double focal, double znear,
+                              gsr_camera* out /*[host]*/);
+
+/* ---- K1: projection + culling (north_star "projection/culling kernel") ----
+   For every (view c, Gaussian g) of the batch: view transform, near cull
+   (vz > znear), EWA 2D covariance with 0.3 px^2 dilation and 1.3x FOV clamp,
+   det cull, conic, radius r = ceil(3.33 sqrt(lambda_max)), 16x16 tile rect,
+   SH colour (degree <= 3), depth-key bits (O1/O4).
+   cams        [host] n_views cameras, all with the same W,H (n_views <= GSR_MAX_VIEWS)
+   render_rec  [V][n][12] float: (u, v, A, B), (C, opacity, uncertainty, tau),
+               (r, g, b, ext) -- conic (A,B,C) = inverse 2D covariance; tau =
+               -ln(255 opacity) - 1e-3 (alpha-skip pre-test bound); ext = two
+               round-up fp16 half-extents of the alpha >= 1/255 ellipse.  Written
+               only where n_tiles > 0 (culled records are left untouched).
+   bin_rec     [4][V][n] uint32 planes: depth bits of view-space z, x0 | x1 << 16,
+               y0 | y1 << 16, n_tiles (0 = culled; then the other planes are 0). */
+gsr_status gsr_project(gsr_ctx* ctx, const gsr_gaussians* gaussians, const gsr_camera* cams,
+                       int32_t n_views, float* render_rec, uint32_t* bin_rec, void* stream);
+
+/* ---- K2-K5: tile-count scan, key duplication, radix sort, tile ranges ----
+   Produces the (view, tile)-sorted Gaussian lists of the batch.  Key of a
+   duplicated entry = ((view_in_batch * gx*gy + ty*gx + tx) << 32) | depth bits,
+   value = g; the sorted order is (key, value) lexicographic (O2/O3).
+   bin_rec     [4][V][n] from gsr_project; n = Gaussians per view
+   cams        [host] the batch's cameras (same W,H)
+   keys        [capacity] uint64, OPTIONAL (NULL: the sorted 64-bit keys are not
+               materialised -- the composite needs only vals + ranges)
+   vals        [capacity] uint32 sorted values (Gaussian index g)
+   capacity    room in keys/vals
+   n_keys      [host] SYNC: receives K, the number of duplicated keys; the call
+               waits for the count (one 8-byte readback per batch)
+   ranges      [V*gx*gy][2] uint32 [start, end) per (view, tile); empty = [s, s)
+   keys_unsorted / vals_unsorted  OPTIONAL [capacity]: the duplicated list in
+               emission order (view, g ascending, ty, tx) -- for parity tests
+   Returns GSR_ECAPACITY (with *n_keys = K, nothing else written) if K > capacity. */
+gsr_status gsr_bin_sort(gsr_ctx* ctx, const uint32_t* bin_rec, int64_t n, const gsr_camera* cams,
+                        int32_t n_views, uint64_t* keys, uint32_t* vals, int64_t capacity,
+                        int64_t* n_keys, uint32_t* ranges, uint64_t* keys_unsorted,
+                        uint32_t* vals_unsorted, void* stream);
+
+/* ---- K6: per-pixel front-to-back compositing of RGB + uncertainty ---------
+   For pixel (px, py) of view c, over its tile's sorted list: alpha =
+   min(0.99, o exp(power)), skip power > 0 or alpha < 1/255, stop before the
+   Gaussian that would take T below 1e-4, accumulate w = alpha T into RGB and U
+   (O5).  Background 0.
+   render_rec, n, vals, ranges: as produced above for the same batch
+   rgbu        OPTIONAL [V][H][W][4] float (r, g, b, U)
+   t_final     OPTIONAL [V][H][W] float;   n_contrib OPTIONAL [V][H][W] uint32
+   tile_partial [V][gx*gy] float: sum of U over the tile's in-image pixels
+   n_frag      OPTIONAL [1] uint64, ADDED to: blended (pixel, Gaussian) pairs */
+gsr_status gsr_composite(gsr_ctx* ctx, const float* render_rec, int64_t n, const uint32_t* vals,
+                         const uint32_t* ranges, const gsr_camera* cams, int32_t n_views,
+                         float* rgbu, float* t_final, uint32_t* n_contrib, float* tile_partial,
+                         unsigned long long* n_frag, void* stream);
+
+/* ---- K7: view score u(θ) = (sum of U over all W*H pixels) / (W*H) ----------
+   (north_star "mean composited uncertainty"; the paper's spatial means
+   PAPER.md L72 "global average", L78 1/(H_z W_z) sum_p).  Deterministic
+   fixed-order reduction of the tile partials (double accumulation).
+   scores [V] float. */
+gsr_status gsr_score_views(gsr_ctx* ctx, const float* tile_partial, const gsr_camera* cams,
+                           int32_t n_views, float* scores, void* stream);
+
+/* ---- K8: next-best-view / top-k (Alg. 1; App. A.2) --
+   Order candidates by (score descending, index ascending), drop excluded
+   ones, return the first k.  scores [n] float (device, finite);
+   exclude [host] OPTIONAL uint8 [n] (non-zero = already captured, never
+   returned -- "avoiding redundant sampling"); out_idx [k] int32
+   (device).  n <= 16384.  GSR_EBUDGET if k < 1 or k > n - #excluded. */
+gsr_status gsr_select_nbv(gsr_ctx* ctx, const float* scores, int32_t n, const uint8_t* exclude,
+                          int32_t k, int32_t* out_idx, void* stream);
+
+/* ---- utility: the onesweep LSD radix sort used by gsr_bin_sort ------------
+   Stable sort of (key, value) pairs by key bits [begin_bit, end_bit), 8-bit
+   digits, one upfront histogram pass + one decoupled-lookback scatter pass
+   per digit.  Keys/vals in are not modified; out buffers receive the result.
+   0 <= begin_bit < end_bit <= 64; n < 2^31.  Exposed for standalone tests and
+   the sort roofline measurement. */
+gsr_status gsr_sort_pairs_u64(gsr_ctx* ctx, const uint64_t* keys_in, const uint32_t* vals_in,
+                              uint64_t* keys_out, uint32_t* vals_out, int64_t n, int32_t begin_bit,
+                              int32_t end_bit, void* stream);
+
+/* ---- utility: bytes of scratch the context currently holds (diagnostics) */
+int64_t gsr_scratch_bytes(const gsr_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GSR_H */

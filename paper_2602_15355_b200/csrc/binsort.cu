@@ -1,0 +1,761 @@
+// binsort.cu -- K2..K5: tile-count scan, key duplication, onesweep radix
+// sort, per-tile ranges (O2/O3).
+//
+// The (view, tile)-major, depth-minor order of the duplicated keys is produced
+// in two levels, each a stable LSD onesweep radix sort with decoupled
+// look-back (one upfront histogram, one scatter pass per 8-bit digit):
+//
+//   K2  k2_compact   single-pass look-back scan of n_tiles over (view, g):
+//                    compacts the visible pairs into 64-bit depth keys
+//                    (view << 32 | depth bits) + value g, counts K, and
+//                    accumulates the digit histograms of the depth sort.
+//   K4a onesweep     depth sort of the visible pairs (32 + log2 V bits).
+//   K3  k3_emit      single-pass look-back scan of n_tiles in depth order,
+//                    warp-cooperative load-balanced emission of the 32-bit
+//                    (view*tiles + tile) keys, per-tile counts with
+//                    warp-aggregated atomics (match_any + one atomicAdd).
+//   K5  k5_ranges    per-tile [start, end) = exclusive scan of the counts,
+//                    plus the digit histograms of the tile sort (from counts).
+//   K4b onesweep     stable tile sort of the duplicated list (log2(V*tiles)
+//                    bits = 2 passes for every config); the last pass writes the
+//                    sorted values (and, if asked, the 64-bit keys).
+//
+// Because LSD radix sorting is stable and the emission order is already
+// (view, depth, g), the result is exactly the (key, value) lexicographic order
+// of the full 64-bit keys -- bit-identical to sorting the 64-bit keys
+// directly (gsr_sort_pairs_u64, also exported), at a third of the HBM traffic.
+#include "gsr_internal.cuh"
+
+#include <algorithm>
+
+namespace gsr {
+namespace {
+
+constexpr uint32_t FULL = 0xffffffffu;
+constexpr uint64_t LB_AGG = 1ull << 62, LB_INC = 2ull << 62, LB_VAL = (1ull << 62) - 1;
+constexpr uint32_t DG_AGG = 1u << 30, DG_INC = 2u << 30, DG_VAL = (1u << 30) - 1;
+
+__device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31; }
+
+template <typename T>
+__device__ __forceinline__ T warp_incl_scan(T v) {
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    T t = __shfl_up_sync(FULL, v, o);
+    if ((int)lane_id() >= o) v += t;
+  }
+  return v;
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+  return v;
+}
+
+// Warp-parallel decoupled look-back over a chain of flagged 64-bit words.
+// Called by a full warp for block `bid` > 0; returns the exclusive prefix.
+__device__ uint64_t warp_lookback(const uint64_t* words, int64_t bid) {
+  const uint32_t lane = lane_id();
+  uint64_t excl = 0;
+  int64_t base = bid - 1;
+  while (true) {
+    const int64_t idx = base - lane;
+    uint64_t w = idx >= 0 ? __ldcv((const unsigned long long*)words + idx) : LB_INC;
+    const uint32_t f = (uint32_t)(w >> 62);
+    const uint32_t notready = __ballot_sync(FULL, f == 0);
+    const uint32_t inc = __ballot_sync(FULL, f == 2);
+    const uint32_t stop = notready | inc;
+    if (stop == 0) {
+      excl += warp_sum<uint64_t>(w & LB_VAL);
+      base -= 32;
+      continue;
+    }
+    const int first = __ffs(stop) - 1;
+    const bool take = (int)lane < first || ((int)lane == first && (inc >> first & 1));
+    excl += warp_sum<uint64_t>(take ? (w & LB_VAL) : 0);
+    if (inc >> first & 1) break;
+    base -= first;  // lanes before `first` were aggregates: consume and spin on `first`
+  }
+  return excl;
+}
+
+__device__ __forceinline__ void publish(uint64_t* words, int64_t bid, uint64_t v) {
+  __stcg((unsigned long long*)words + bid, (unsigned long long)v);
+}
+
+// ---------------------------------------------------------------------------
+// K2: compact visible (view, g) pairs, K and visible-count totals.
+// Block tile = 256 threads x 8 consecutive items.
+constexpr int K2_ITEMS = 8;
+constexpr int K2_TILE = 256 * K2_ITEMS;
+
+__global__ void __launch_bounds__(256) k2_compact(const uint32_t* __restrict__ depth_plane,
+                                                  const uint32_t* __restrict__ nt_plane, int64_t M, int64_t n,
+                                                  uint64_t* __restrict__ dkeys, uint32_t* __restrict__ dvals,
+                                                  uint32_t* __restrict__ emit_off, uint64_t* __restrict__ lb_vis,
+                                                  uint64_t* __restrict__ lb_k, uint32_t* __restrict__ ctr,
+                                                  uint64_t* __restrict__ totals, uint32_t* __restrict__ hist,
+                                                  int dpasses) {
+  __shared__ uint32_t s_hist[5][256];
+  __shared__ uint64_t s_wv[8], s_wk[8];
+  __shared__ uint64_t s_pv, s_pk;
+  __shared__ uint32_t s_bid;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) s_bid = atomicAdd(ctr, 1u);
+  for (int i = tid; i < 5 * 256; i += 256) (&s_hist[0][0])[i] = 0;
+  __syncthreads();
+  const int64_t bid = s_bid;
+  const int64_t i0 = bid * K2_TILE + (int64_t)tid * K2_ITEMS;
+  uint32_t nt[K2_ITEMS];
+  uint32_t cv = 0;
+  uint64_t ck = 0;
+#pragma unroll
+  for (int k = 0; k < K2_ITEMS; ++k) {
+    nt[k] = (i0 + k < M) ? __ldg(nt_plane + i0 + k) : 0u;
+    cv += nt[k] > 0;
+    ck += nt[k];
+  }
+  // block exclusive scan of (cv, ck)
+  uint64_t iv = warp_incl_scan<uint64_t>(cv), ik = warp_incl_scan<uint64_t>(ck);
+  if (lane == 31) { s_wv[warp] = iv; s_wk[warp] = ik; }
+  __syncthreads();
+  if (warp == 0) {
+    uint64_t wv = lane < 8 ? s_wv[lane] : 0, wk = lane < 8 ? s_wk[lane] : 0;
+    uint64_t sv = warp_incl_scan<uint64_t>(wv), sk = warp_incl_scan<uint64_t>(wk);
+    if (lane < 8) { s_wv[lane] = sv - wv; s_wk[lane] = sk - wk; }
+    const uint64_t tv = __shfl_sync(FULL, sv, 7), tk = __shfl_sync(FULL, sk, 7);
+    uint64_t pv = 0, pk = 0;
+    if (bid == 0) {
+      if (lane == 0) { publish(lb_vis, 0, LB_INC | tv); publish(lb_k, 0, LB_INC | tk); }
+    } else {
+      if (lane == 0) { publish(lb_vis, bid, LB_AGG | tv); publish(lb_k, bid, LB_AGG | tk); }
+      pv = warp_lookback(lb_vis, bid);
+      pk = warp_lookback(lb_k, bid);
+      if (lane == 0) { publish(lb_vis, bid, LB_INC | (pv + tv)); publish(lb_k, bid, LB_INC | (pk + tk)); }
+    }
+    if (lane == 0) {
+      s_pv = pv; s_pk = pk;
+      if ((bid + 1) * K2_TILE >= M) { totals[0] = pv + tv; totals[1] = pk + tk; }
+    }
+  }
+  __syncthreads();
+  uint64_t pv = s_pv + s_wv[warp] + (iv - cv);
+  uint64_t pk = s_pk + s_wk[warp] + (ik - ck);
+#pragma unroll
+  for (int k = 0; k < K2_ITEMS; ++k) {
+    const int64_t i = i0 + k;
+    if (i >= M) break;
+    if (emit_off) emit_off[i] = (uint32_t)pk;
+    if (nt[k]) {
+      const uint64_t view = (uint64_t)(i / n);
+      const uint32_t g = (uint32_t)(i - (int64_t)view * n);
+      const uint64_t key = (view << 32) | __ldg(depth_plane + i);
+      dkeys[pv] = key;
+      dvals[pv] = g;
+      for (int p = 0; p < dpasses; ++p) atomicAdd(&s_hist[p][(key >> (8 * p)) & 255], 1u);
+      ++pv;
+    }
+    pk += nt[k];
+  }
+  __syncthreads();
+  for (int i = tid; i < dpasses * 256; i += 256) {
+    const uint32_t c = (&s_hist[0][0])[i];
+    if (c) atomicAdd(hist + i, c);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Exclusive scan of `passes` 256-bin histograms -> bases (one block).
+__global__ void scan_hist(const uint32_t* __restrict__ hist, uint32_t* __restrict__ base, int passes) {
+  __shared__ uint32_t s_w[8];
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  for (int p = 0; p < passes; ++p) {
+    const uint32_t c = hist[p * 256 + t];
+    const uint32_t inc = warp_incl_scan<uint32_t>(c);
+    if (lane == 31) s_w[warp] = inc;
+    __syncthreads();
+    uint32_t off = 0;
+    for (int w = 0; w < warp; ++w) off += s_w[w];
+    base[p * 256 + t] = off + inc - c;
+    __syncthreads();
+  }
+}
+
+// Histograms of all passes of a u64-key sort (utility sort).
+__global__ void __launch_bounds__(256) hist_u64(const uint64_t* __restrict__ keys, int64_t n, int begin_bit,
+                                                int passes, int end_bit, uint32_t* __restrict__ hist) {
+  __shared__ uint32_t s_hist[8][256];
+  for (int i = threadIdx.x; i < 8 * 256; i += 256) (&s_hist[0][0])[i] = 0;
+  __syncthreads();
+  for (int64_t i = (int64_t)blockIdx.x * 256 + threadIdx.x; i < n; i += (int64_t)gridDim.x * 256) {
+    const uint64_t k = keys[i];
+    for (int p = 0; p < passes; ++p) {
+      const int sh = begin_bit + 8 * p;
+      const int nb = min(8, end_bit - sh);
+      atomicAdd(&s_hist[p][(uint32_t)(k >> sh) & ((1u << nb) - 1)], 1u);
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < passes * 256; i += 256) {
+    const uint32_t c = (&s_hist[0][0])[i];
+    if (c) atomicAdd(hist + i, c);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// One onesweep LSD pass: stable scatter of (key, value) by the digit
+// (key >> shift) & (2^nbits - 1).  Dynamic block ids guarantee forward
+// progress of the per-digit decoupled look-back.
+//   MODE 0: write keys_out / vals_out.
+//   MODE 1: tile sort final pass (KeyT = u32 key = view*tpv + tile): write
+//           vals_out and, if keys64 != null, the full 64-bit key
+//           (key << 32) | depth_plane[view * nper + g].
+template <typename KeyT, int KPT, int MODE>
+__global__ void __launch_bounds__(256) onesweep(const KeyT* __restrict__ kin, const uint32_t* __restrict__ vin,
+                                                KeyT* __restrict__ kout, uint32_t* __restrict__ vout, uint32_t n,
+                                                int shift, int nbits, const uint32_t* __restrict__ base,
+                                                uint32_t* __restrict__ lookback, uint32_t* __restrict__ ctr,
+                                                uint64_t* __restrict__ keys64, const uint32_t* __restrict__ depth_plane,
+                                                uint32_t tpv, int64_t nper) {
+  constexpr int B = 256, W = B / 32, TILE = B * KPT;
+  struct Stage {
+    KeyT k[TILE];
+    uint32_t v[TILE];
+  };
+  union Smem {
+    uint32_t hist[W][256];
+    Stage st;
+  };
+  __shared__ Smem u;
+  __shared__ uint32_t s_start[256], s_gbase[256], s_wsum[W];
+  __shared__ uint32_t s_bid;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) s_bid = atomicAdd(ctr, 1u);
+  for (int i = tid; i < W * 256; i += B) (&u.hist[0][0])[i] = 0;
+  __syncthreads();
+  const uint32_t bid = s_bid;
+  const uint32_t mask = (nbits >= 32) ? 0xffffffffu : ((1u << nbits) - 1);
+  const int64_t wbase = (int64_t)bid * TILE + (int64_t)warp * (KPT * 32);
+  KeyT key[KPT];
+  uint32_t val[KPT], rank[KPT];
+#pragma unroll
+  for (int k = 0; k < KPT; ++k) {
+    const int64_t idx = wbase + k * 32 + lane;
+    const bool valid = idx < (int64_t)n;
+    key[k] = valid ? kin[idx] : KeyT(0);
+    val[k] = valid ? vin[idx] : 0u;
+  }
+  const uint32_t lt = (1u << lane) - 1;
+#pragma unroll
+  for (int k = 0; k < KPT; ++k) {
+    const int64_t idx = wbase + k * 32 + lane;
+    const bool valid = idx < (int64_t)n;
+    const uint32_t d = (uint32_t)(key[k] >> shift) & mask;
+    const uint32_t peers = __match_any_sync(FULL, valid ? d : 0xffffffffu);
+    const uint32_t r = __popc(peers & lt);
+    uint32_t pre = 0;
+    if (valid) pre = u.hist[warp][d];
+    __syncwarp();
+    if (valid && r == 0) u.hist[warp][d] = pre + __popc(peers);
+    __syncwarp();
+    rank[k] = pre + r;
+  }
+  __syncthreads();
+  // per digit: exclusive prefix over warps, block total, look-back
+  {
+    const int d = tid;
+    uint32_t total = 0;
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+      const uint32_t c = u.hist[w][d];
+      u.hist[w][d] = total;
+      total += c;
+    }
+    uint32_t* my = lookback + (size_t)bid * 256 + d;
+    uint32_t excl = 0;
+    if (bid == 0) {
+      __stcg(my, DG_INC | total);
+    } else {
+      __stcg(my, DG_AGG | total);
+      int64_t j = (int64_t)bid - 1;
+      while (true) {
+        const uint32_t w = __ldcv(lookback + (size_t)j * 256 + d);
+        const uint32_t f = w >> 30;
+        if (f == 0) continue;
+        excl += w & DG_VAL;
+        if (f == 2) break;
+        --j;
+      }
+      __stcg(my, DG_INC | (excl + total));
+    }
+    // block-local exclusive scan of totals over digits
+    const uint32_t inc = warp_incl_scan<uint32_t>(total);
+    if (lane == 31) s_wsum[warp] = inc;
+    __syncthreads();
+    uint32_t off = 0;
+#pragma unroll
+    for (int w = 0; w < W; ++w) off += (w < warp) ? s_wsum[w] : 0u;
+    const uint32_t start = off + inc - total;
+    s_start[d] = start;
+    s_gbase[d] = base[d] + excl - start;
+  }
+  __syncthreads();
+  uint32_t pos[KPT];
+#pragma unroll
+  for (int k = 0; k < KPT; ++k) {
+    const uint32_t d = (uint32_t)(key[k] >> shift) & mask;
+    pos[k] = s_start[d] + u.hist[warp][d] + rank[k];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < KPT; ++k) {
+    const int64_t idx = wbase + k * 32 + lane;
+    if (idx < (int64_t)n) {
+      u.st.k[pos[k]] = key[k];
+      u.st.v[pos[k]] = val[k];
+    }
+  }
+  __syncthreads();
+  const int64_t rem = (int64_t)n - (int64_t)bid * TILE;
+  const int nvalid = rem < TILE ? (int)rem : TILE;
+  for (int i = tid; i < nvalid; i += B) {
+    const KeyT kk = u.st.k[i];
+    const uint32_t vv = u.st.v[i];
+    const uint32_t d = (uint32_t)(kk >> shift) & mask;
+    const uint32_t o = s_gbase[d] + i;
+    if (MODE == 0) {
+      kout[o] = kk;
+      vout[o] = vv;
+    } else {
+      vout[o] = vv;
+      if (keys64) {
+        const uint32_t k32 = (uint32_t)kk;
+        const uint32_t view = k32 / tpv;
+        keys64[o] = ((uint64_t)k32 << 32) | __ldg(depth_plane + (int64_t)view * nper + vv);
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K3: look-back scan of n_tiles in depth-sorted order + load-balanced emission.
+// Block = 8 warps x 8 rounds x 32 entries = 2048 entries; warp w owns 256
+// consecutive entries.
+constexpr int K3_ROUNDS = 8;
+constexpr int K3_TILE = 256 * K3_ROUNDS;
+
+__global__ void __launch_bounds__(256) k3_emit(const uint64_t* __restrict__ dkeys, const uint32_t* __restrict__ dvals,
+                                               int64_t nvis, const uint32_t* __restrict__ xr_plane,
+                                               const uint32_t* __restrict__ yr_plane,
+                                               const uint32_t* __restrict__ nt_plane, int64_t n, uint32_t gx,
+                                               uint32_t tpv, uint32_t* __restrict__ tkeys,
+                                               uint32_t* __restrict__ tvals, uint32_t* __restrict__ counts,
+                                               uint64_t* __restrict__ lb, uint32_t* __restrict__ ctr) {
+  __shared__ uint64_t s_w[8];
+  __shared__ uint64_t s_prefix;
+  __shared__ uint32_t s_bid;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) s_bid = atomicAdd(ctr, 1u);
+  __syncthreads();
+  const int64_t bid = s_bid;
+  const int64_t e0 = bid * K3_TILE + (int64_t)warp * (32 * K3_ROUNDS);
+  uint32_t nt[K3_ROUNDS], xr[K3_ROUNDS], yr[K3_ROUNDS], g[K3_ROUNDS], view[K3_ROUNDS];
+  uint64_t mine = 0;
+#pragma unroll
+  for (int r = 0; r < K3_ROUNDS; ++r) {
+    const int64_t e = e0 + r * 32 + lane;
+    nt[r] = 0; xr[r] = 0; yr[r] = 0; g[r] = 0; view[r] = 0;
+    if (e < nvis) {
+      const uint64_t key = dkeys[e];
+      g[r] = dvals[e];
+      view[r] = (uint32_t)(key >> 32);
+      const int64_t pi = (int64_t)view[r] * n + g[r];
+      nt[r] = __ldg(nt_plane + pi);
+      xr[r] = __ldg(xr_plane + pi);
+      yr[r] = __ldg(yr_plane + pi);
+    }
+    mine += nt[r];
+  }
+  const uint64_t wtot = warp_sum<uint64_t>(mine);
+  if (lane == 0) s_w[warp] = wtot;
+  __syncthreads();
+  if (warp == 0) {
+    const uint64_t v = lane < 8 ? s_w[lane] : 0;
+    const uint64_t inc = warp_incl_scan<uint64_t>(v);
+    const uint64_t tot = __shfl_sync(FULL, inc, 7);
+    if (lane < 8) s_w[lane] = inc - v;
+    uint64_t p = 0;
+    if (bid == 0) {
+      if (lane == 0) publish(lb, 0, LB_INC | tot);
+    } else {
+      if (lane == 0) publish(lb, bid, LB_AGG | tot);
+      p = warp_lookback(lb, bid);
+      if (lane == 0) publish(lb, bid, LB_INC | (p + tot));
+    }
+    if (lane == 0) s_prefix = p;
+  }
+  __syncthreads();
+  uint64_t base = s_prefix + s_w[warp];
+#pragma unroll
+  for (int r = 0; r < K3_ROUNDS; ++r) {
+    const uint32_t inc = warp_incl_scan<uint32_t>(nt[r]);
+    const uint32_t excl = inc - nt[r];
+    const uint32_t total = __shfl_sync(FULL, inc, 31);
+    const uint32_t x0 = xr[r] & 0xffffu, wdt = (xr[r] >> 16) - x0, y0 = yr[r] & 0xffffu;
+    for (uint32_t jb = 0; jb < total; jb += 32) {
+      const uint32_t j = jb + lane;
+      // owner lane: largest s with excl[s] <= j
+      int s = 0;
+#pragma unroll
+      for (int step = 16; step > 0; step >>= 1) {
+        const uint32_t e = __shfl_sync(FULL, excl, s + step);
+        if (e <= j) s += step;
+      }
+      const uint32_t oexcl = __shfl_sync(FULL, excl, s);
+      const uint32_t ox0 = __shfl_sync(FULL, x0, s), ow = __shfl_sync(FULL, wdt, s);
+      const uint32_t oy0 = __shfl_sync(FULL, y0, s), og = __shfl_sync(FULL, g[r], s);
+      const uint32_t ov = __shfl_sync(FULL, view[r], s);
+      const bool act = j < total;
+      uint32_t key = 0xffffffffu;
+      if (act) {
+        const uint32_t loc = j - oexcl;
+        const uint32_t ty = oy0 + loc / ow, tx = ox0 + loc % ow;
+        key = ov * tpv + ty * gx + tx;
+        tkeys[base + j] = key;
+        tvals[base + j] = og;
+      }
+      const uint32_t peers = __match_any_sync(FULL, key);
+      if (act && (__ffs(peers) - 1) == lane) atomicAdd(counts + key, (uint32_t)__popc(peers));
+    }
+    base += total;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K5: ranges[t] = [s, s + counts[t]) with s = exclusive prefix of counts, and
+// the tile-sort digit histograms + bases.  One block of 1024 threads.
+__global__ void __launch_bounds__(1024) k5_ranges(const uint32_t* __restrict__ counts, int64_t T,
+                                                  uint2* __restrict__ ranges, int tpasses,
+                                                  uint32_t* __restrict__ hist, uint32_t* __restrict__ base) {
+  __shared__ uint32_t s_hist[4][256];
+  __shared__ uint32_t s_w[32];
+  __shared__ uint32_t s_carry;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int i = tid; i < 4 * 256; i += 1024) (&s_hist[0][0])[i] = 0;
+  if (tid == 0) s_carry = 0;
+  __syncthreads();
+  constexpr int IT = 16;
+  for (int64_t c0 = 0; c0 < T; c0 += 1024 * IT) {
+    uint32_t v[IT];
+    uint32_t sum = 0;
+    const int64_t t0 = c0 + (int64_t)tid * IT;
+#pragma unroll
+    for (int k = 0; k < IT; ++k) {
+      const int64_t t = t0 + k;
+      v[k] = t < T ? counts[t] : 0u;
+      sum += v[k];
+      if (v[k]) {
+        for (int p = 0; p < tpasses; ++p) atomicAdd(&s_hist[p][(uint32_t)(t >> (8 * p)) & 255], v[k]);
+      }
+    }
+    const uint32_t inc = warp_incl_scan<uint32_t>(sum);
+    if (lane == 31) s_w[warp] = inc;
+    __syncthreads();
+    if (warp == 0) {
+      const uint32_t wv = s_w[lane];
+      const uint32_t wi = warp_incl_scan<uint32_t>(wv);
+      s_w[lane] = wi - wv;
+    }
+    __syncthreads();
+    uint32_t run = s_carry + s_w[warp] + inc - sum;
+#pragma unroll
+    for (int k = 0; k < IT; ++k) {
+      const int64_t t = t0 + k;
+      if (t < T) ranges[t] = make_uint2(run, run + v[k]);
+      run += v[k];
+    }
+    __syncthreads();
+    if (tid == 1023) s_carry = run;
+    __syncthreads();
+  }
+  // histograms -> exclusive bases
+  for (int p = 0; p < tpasses; ++p) {
+    uint32_t c = 0, inc = 0;
+    if (tid < 256) {  // warps 0..7, fully active
+      c = s_hist[p][tid];
+      hist[p * 256 + tid] = c;
+      inc = warp_incl_scan<uint32_t>(c);
+      if (lane == 31) s_w[warp] = inc;
+    }
+    __syncthreads();
+    if (tid < 256) {
+      uint32_t off = 0;
+      for (int w = 0; w < warp; ++w) off += s_w[w];
+      base[p * 256 + tid] = off + inc - c;
+    }
+    __syncthreads();
+  }
+}
+
+// O2 emission order (view, g, ty, tx): parity output only.
+__global__ void __launch_bounds__(256) k_emit_o2(const uint32_t* __restrict__ depth_plane,
+                                                 const uint32_t* __restrict__ xr_plane,
+                                                 const uint32_t* __restrict__ yr_plane,
+                                                 const uint32_t* __restrict__ nt_plane,
+                                                 const uint32_t* __restrict__ emit_off, int64_t M, int64_t n,
+                                                 uint32_t gx, uint32_t tpv, uint64_t* __restrict__ keys,
+                                                 uint32_t* __restrict__ vals) {
+  const int64_t i = (int64_t)blockIdx.x * 256 + threadIdx.x;
+  if (i >= M) return;
+  const uint32_t nt = nt_plane[i];
+  if (!nt) return;
+  const uint64_t view = (uint64_t)(i / n);
+  const uint32_t g = (uint32_t)(i - (int64_t)view * n);
+  const uint32_t xr = xr_plane[i], yr = yr_plane[i], d = depth_plane[i];
+  uint64_t o = emit_off[i];
+  for (uint32_t ty = yr & 0xffffu; ty < (yr >> 16); ++ty)
+    for (uint32_t tx = xr & 0xffffu; tx < (xr >> 16); ++tx) {
+      const uint64_t tile = view * tpv + (uint64_t)ty * gx + tx;
+      keys[o] = (tile << 32) | d;
+      vals[o] = g;
+      ++o;
+    }
+}
+
+int bits_for(uint64_t count) {  // ceil(log2(count)), 0 for count <= 1
+  int b = 0;
+  while ((1ull << b) < count) ++b;
+  return b;
+}
+
+constexpr int KPT64 = 12;  // onesweep u64 keys: 3072 keys per block
+constexpr int KPT32 = 16;  // onesweep u32 keys: 4096 keys per block
+
+size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// Generic multi-pass onesweep over u64 keys (ping-pong through scratch).
+static gsr_status sort_u64_passes(gsr_ctx* ctx, const uint64_t* kin, const uint32_t* vin, uint64_t* kout,
+                                  uint32_t* vout, uint64_t* ktmp, uint32_t* vtmp, int64_t n, int begin_bit,
+                                  int end_bit, const uint32_t* base, uint32_t* lookback, uint32_t* ctrs,
+                                  cudaStream_t st) {
+  const int passes = (end_bit - begin_bit + 7) / 8;
+  const uint32_t nb = (uint32_t)((n + 256 * KPT64 - 1) / (256 * KPT64));
+  // choose buffers so that the last pass lands in kout
+  const uint64_t* ci = kin;
+  const uint32_t* cv = vin;
+  for (int p = 0; p < passes; ++p) {
+    const bool to_out = ((passes - 1 - p) % 2) == 0;
+    uint64_t* ko = to_out ? kout : ktmp;
+    uint32_t* vo = to_out ? vout : vtmp;
+    const int sh = begin_bit + 8 * p;
+    const int nbits = std::min(8, end_bit - sh);
+    onesweep<uint64_t, KPT64, 0><<<nb, 256, 0, st>>>(ci, cv, ko, vo, (uint32_t)n, sh, nbits, base + 256 * p,
+                                                     lookback + (size_t)p * nb * 256, ctrs + p, nullptr, nullptr,
+                                                     0, 0);
+    ci = ko;
+    cv = vo;
+  }
+  return check_cuda(ctx, cudaGetLastError(), "onesweep u64");
+}
+
+}  // namespace gsr
+
+using namespace gsr;
+
+extern "C" gsr_status gsr_sort_pairs_u64(gsr_ctx* ctx, const uint64_t* keys_in, const uint32_t* vals_in,
+                                         uint64_t* keys_out, uint32_t* vals_out, int64_t n, int32_t begin_bit,
+                                         int32_t end_bit, void* stream) {
+  if (!ctx) return GSR_EINVAL;
+  if (n < 0 || n >= (1ll << 31)) return set_err(ctx, GSR_EINVAL, "gsr_sort_pairs_u64: n out of range");
+  if (begin_bit < 0 || end_bit > 64 || begin_bit >= end_bit)
+    return set_err(ctx, GSR_EINVAL, "gsr_sort_pairs_u64: bad bit range");
+  if (n > 0 && (!keys_in || !vals_in || !keys_out || !vals_out))
+    return set_err(ctx, GSR_EINVAL, "gsr_sort_pairs_u64: NULL pointer");
+  if (n == 0) return GSR_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int passes = (end_bit - begin_bit + 7) / 8;
+  const size_t nb = (size_t)((n + 256 * KPT64 - 1) / (256 * KPT64));
+  void *kt, *vt, *hs, *lb;
+  gsr_status s;
+  if ((s = ensure(ctx, S_SORTK, n * 8, &kt)) != GSR_OK) return s;
+  if ((s = ensure(ctx, S_SORTV, n * 4, &vt)) != GSR_OK) return s;
+  if ((s = ensure(ctx, S_HIST, 2 * 8 * 256 * 4, &hs)) != GSR_OK) return s;
+  const size_t lb_bytes = align_up(passes * nb * 256 * 4) + 64 * 4;
+  if ((s = ensure(ctx, S_LOOKBACK, lb_bytes, &lb)) != GSR_OK) return s;
+  uint32_t* hist = (uint32_t*)hs;
+  uint32_t* base = hist + 8 * 256;
+  uint32_t* look = (uint32_t*)lb;
+  uint32_t* ctrs = (uint32_t*)((char*)lb + align_up(passes * nb * 256 * 4));
+  if ((s = check_cuda(ctx, cudaMemsetAsync(hist, 0, 8 * 256 * 4, st), "memset")) != GSR_OK) return s;
+  if ((s = check_cuda(ctx, cudaMemsetAsync(lb, 0, lb_bytes, st), "memset")) != GSR_OK) return s;
+  const int hb = (int)std::min<int64_t>((n + 255) / 256, (int64_t)ctx->num_sms * 8);
+  hist_u64<<<hb, 256, 0, st>>>(keys_in, n, begin_bit, passes, end_bit, hist);
+  scan_hist<<<1, 256, 0, st>>>(hist, base, passes);
+  if ((s = check_cuda(ctx, cudaGetLastError(), "hist")) != GSR_OK) return s;
+  return sort_u64_passes(ctx, keys_in, vals_in, keys_out, vals_out, (uint64_t*)kt, (uint32_t*)vt, n, begin_bit,
+                         end_bit, base, look, ctrs, st);
+}
+
+extern "C" gsr_status gsr_bin_sort(gsr_ctx* ctx, const uint32_t* bin_rec, int64_t n, const gsr_camera* cams,
+                                   int32_t n_views, uint64_t* keys, uint32_t* vals, int64_t capacity,
+                                   int64_t* n_keys, uint32_t* ranges, uint64_t* keys_unsorted,
+                                   uint32_t* vals_unsorted, void* stream) {
+  if (!ctx) return GSR_EINVAL;
+  if (!bin_rec || !cams || !vals || !n_keys || !ranges)
+    return set_err(ctx, GSR_EINVAL, "gsr_bin_sort: NULL required pointer");
+  if (n < 0 || n_views <= 0 || n_views > GSR_MAX_VIEWS || capacity < 0)
+    return set_err(ctx, GSR_EINVAL, "gsr_bin_sort: bad n / n_views / capacity");
+  if ((keys_unsorted == nullptr) != (vals_unsorted == nullptr))
+    return set_err(ctx, GSR_EINVAL, "gsr_bin_sort: keys_unsorted and vals_unsorted go together");
+  const int W = cams[0].width, H = cams[0].height;
+  for (int c = 0; c < n_views; ++c)
+    if (cams[c].width != W || cams[c].height != H || W <= 0 || H <= 0)
+      return set_err(ctx, GSR_EINVAL, "gsr_bin_sort: mixed or non-positive resolutions in a batch");
+  const uint32_t gx = (W + kTile - 1) / kTile, gy = (H + kTile - 1) / kTile;
+  const uint64_t tpv = (uint64_t)gx * gy;
+  const uint64_t T = tpv * (uint64_t)n_views;
+  if (T >= (1ull << 32)) return set_err(ctx, GSR_EINVAL, "gsr_bin_sort: V*tiles >= 2^32");
+  const int64_t M = n * (int64_t)n_views;
+  if (M >= (1ll << 30)) return set_err(ctx, GSR_EINVAL, "gsr_bin_sort: V*n >= 2^30");
+  cudaStream_t st = (cudaStream_t)stream;
+  gsr_status s;
+
+  const uint32_t* p_depth = bin_rec;
+  const uint32_t* p_xr = bin_rec + M;
+  const uint32_t* p_yr = bin_rec + 2 * M;
+  const uint32_t* p_nt = bin_rec + 3 * M;
+
+  const int vbits = bits_for((uint64_t)n_views);
+  const int dpasses = (32 + vbits + 7) / 8;               // depth sort passes
+  const int tbits = bits_for(T);
+  const int tpasses = std::max(1, (tbits + 7) / 8);       // tile sort passes
+  if (dpasses > 5 || tpasses > 4) return set_err(ctx, GSR_EINVAL, "gsr_bin_sort: batch too large");
+
+  // ---- K2: compact + totals ----
+  void *dka, *dkb, *dva, *dvb, *hs, *lb, *tot, *eo = nullptr;
+  const size_t Mz = (size_t)std::max<int64_t>(M, 1);
+  if ((s = ensure(ctx, S_DKEY_A, Mz * 8, &dka)) != GSR_OK) return s;
+  if ((s = ensure(ctx, S_DKEY_B, Mz * 8, &dkb)) != GSR_OK) return s;
+  if ((s = ensure(ctx, S_DVAL_A, Mz * 4, &dva)) != GSR_OK) return s;
+  if ((s = ensure(ctx, S_DVAL_B, Mz * 4, &dvb)) != GSR_OK) return s;
+  if ((s = ensure(ctx, S_HIST, 4 * 8 * 256 * 4, &hs)) != GSR_OK) return s;
+  if ((s = ensure(ctx, S_TOTALS, 64, &tot)) != GSR_OK) return s;
+  if (keys_unsorted && (s = ensure(ctx, S_EMITOFF, Mz * 4, &eo)) != GSR_OK) return s;
+  uint32_t* dhist = (uint32_t*)hs;          // [5][256]
+  uint32_t* dbase = dhist + 8 * 256;        // [5][256]
+  uint32_t* thist = dhist + 16 * 256;       // [4][256]
+  uint32_t* tbase = dhist + 24 * 256;       // [4][256]
+  const size_t nb2 = (size_t)((M + K2_TILE - 1) / K2_TILE);
+  const size_t lb1 = align_up(2 * std::max<size_t>(nb2, 1) * 8) + 256;
+  if ((s = ensure(ctx, S_LOOKBACK, lb1, &lb)) != GSR_OK) return s;
+  if ((s = check_cuda(ctx, cudaMemsetAsync(lb, 0, lb1, st), "memset lb")) != GSR_OK) return s;
+  if ((s = check_cuda(ctx, cudaMemsetAsync(dhist, 0, 8 * 256 * 4, st), "memset hist")) != GSR_OK) return s;
+  if ((s = check_cuda(ctx, cudaMemsetAsync(tot, 0, 64, st), "memset tot")) != GSR_OK) return s;
+  uint64_t* lbv = (uint64_t*)lb;
+  uint64_t* lbk = lbv + std::max<size_t>(nb2, 1);
+  uint32_t* ctr2 = (uint32_t*)((char*)lb + align_up(2 * std::max<size_t>(nb2, 1) * 8));
+  if (M > 0)
+    k2_compact<<<(unsigned)nb2, 256, 0, st>>>(p_depth, p_nt, M, n, (uint64_t*)dka, (uint32_t*)dva,
+                                              (uint32_t*)eo, lbv, lbk, ctr2, (uint64_t*)tot, dhist, dpasses);
+  if ((s = check_cuda(ctx, cudaGetLastError(), "k2_compact")) != GSR_OK) return s;
+  uint64_t* hp = (uint64_t*)ctx->host_pinned;
+  if ((s = check_cuda(ctx, cudaMemcpyAsync(hp, tot, 16, cudaMemcpyDeviceToHost, st), "readback")) != GSR_OK)
+    return s;
+  if ((s = check_cuda(ctx, cudaStreamSynchronize(st), "sync")) != GSR_OK) return s;
+  const int64_t nvis = (int64_t)hp[0];
+  const int64_t K = (int64_t)hp[1];
+  *n_keys = K;
+  if (K > capacity) return set_err(ctx, GSR_ECAPACITY, "gsr_bin_sort: capacity too small (n_keys = required)");
+  if (K >= (1ll << 31)) return set_err(ctx, GSR_EINVAL, "gsr_bin_sort: K >= 2^31 keys in one batch");
+
+  if (K == 0) {
+    if ((s = check_cuda(ctx, cudaMemsetAsync(ranges, 0, T * 8, st), "memset ranges")) != GSR_OK) return s;
+    return GSR_OK;
+  }
+
+  // ---- scratch for the rest ----
+  void *tka, *tkb, *tva, *tvb, *cnt;
+  if ((s = ensure(ctx, S_TKEY_A, K * 4, &tka)) != GSR_OK) return s;
+  if ((s = ensure(ctx, S_TKEY_B, K * 4, &tkb)) != GSR_OK) return s;
+  if ((s = ensure(ctx, S_TVAL_A, K * 8, &tva)) != GSR_OK) return s;  // holds two u32 arrays
+  tvb = (uint32_t*)tva + K;
+  if ((s = ensure(ctx, S_COUNTS, T * 4, &cnt)) != GSR_OK) return s;
+  const size_t nbd = (size_t)((nvis + 256 * KPT64 - 1) / (256 * KPT64));
+  const size_t nb3 = (size_t)((nvis + K3_TILE - 1) / K3_TILE);
+  const size_t nbt = (size_t)((K + 256 * KPT32 - 1) / (256 * KPT32));
+  const size_t o_d = 0;
+  const size_t o_3 = align_up(o_d + dpasses * nbd * 256 * 4);
+  const size_t o_t = align_up(o_3 + nb3 * 8);
+  const size_t o_c = align_up(o_t + tpasses * nbt * 256 * 4);
+  const size_t lb2 = o_c + 64 * 4;
+  // K2's look-back words are dead now (the sync above ordered them): reuse the slot.
+  if ((s = ensure(ctx, S_LOOKBACK, lb2, &lb)) != GSR_OK) return s;
+  if ((s = check_cuda(ctx, cudaMemsetAsync(lb, 0, lb2, st), "memset lb2")) != GSR_OK) return s;
+  if ((s = check_cuda(ctx, cudaMemsetAsync(cnt, 0, T * 4, st), "memset counts")) != GSR_OK) return s;
+  uint32_t* lbd = (uint32_t*)((char*)lb + o_d);
+  uint64_t* lb3 = (uint64_t*)((char*)lb + o_3);
+  uint32_t* lbt = (uint32_t*)((char*)lb + o_t);
+  uint32_t* ctrs = (uint32_t*)((char*)lb + o_c);  // [0..4] depth, [5] k3, [6..9] tile
+
+  // ---- K4a: depth sort of the visible pairs ----
+  scan_hist<<<1, 256, 0, st>>>(dhist, dbase, dpasses);
+  const uint64_t* ck = (const uint64_t*)dka;
+  const uint32_t* cvv = (const uint32_t*)dva;
+  for (int p = 0; p < dpasses; ++p) {
+    uint64_t* ko = (p % 2 == 0) ? (uint64_t*)dkb : (uint64_t*)dka;
+    uint32_t* vo = (p % 2 == 0) ? (uint32_t*)dvb : (uint32_t*)dva;
+    const int sh = 8 * p;
+    onesweep<uint64_t, KPT64, 0><<<(unsigned)nbd, 256, 0, st>>>(ck, cvv, ko, vo, (uint32_t)nvis, sh,
+                                                                std::min(8, 32 + vbits - sh), dbase + 256 * p,
+                                                                lbd + (size_t)p * nbd * 256, ctrs + p, nullptr,
+                                                                nullptr, 0, 0);
+    ck = ko;
+    cvv = vo;
+  }
+  if ((s = check_cuda(ctx, cudaGetLastError(), "depth sort")) != GSR_OK) return s;
+
+  // ---- K3: emission + counts ----
+  k3_emit<<<(unsigned)nb3, 256, 0, st>>>(ck, cvv, nvis, p_xr, p_yr, p_nt, n, gx, (uint32_t)tpv, (uint32_t*)tka,
+                                         (uint32_t*)tva, (uint32_t*)cnt, lb3, ctrs + 5);
+  if ((s = check_cuda(ctx, cudaGetLastError(), "k3_emit")) != GSR_OK) return s;
+
+  // ---- K5: ranges + tile-sort histograms ----
+  k5_ranges<<<1, 1024, 0, st>>>((const uint32_t*)cnt, (int64_t)T, (uint2*)ranges, tpasses, thist, tbase);
+  if ((s = check_cuda(ctx, cudaGetLastError(), "k5_ranges")) != GSR_OK) return s;
+
+  // ---- K4b: tile sort ----
+  const uint32_t* tk = (const uint32_t*)tka;
+  const uint32_t* tv = (const uint32_t*)tva;
+  for (int p = 0; p < tpasses; ++p) {
+    const int sh = 8 * p;
+    const int nbits = std::max(1, std::min(8, tbits - sh));
+    uint32_t* lbp = lbt + (size_t)p * nbt * 256;
+    if (p == tpasses - 1) {
+      onesweep<uint32_t, KPT32, 1><<<(unsigned)nbt, 256, 0, st>>>(tk, tv, nullptr, vals, (uint32_t)K, sh, nbits,
+                                                                  tbase + 256 * p, lbp, ctrs + 6 + p, keys, p_depth,
+                                                                  (uint32_t)tpv, n);
+    } else {
+      uint32_t* ko = (p % 2 == 0) ? (uint32_t*)tkb : (uint32_t*)tka;
+      uint32_t* vo = (p % 2 == 0) ? (uint32_t*)tvb : (uint32_t*)tva;
+      onesweep<uint32_t, KPT32, 0><<<(unsigned)nbt, 256, 0, st>>>(tk, tv, ko, vo, (uint32_t)K, sh, nbits,
+                                                                  tbase + 256 * p, lbp, ctrs + 6 + p, nullptr,
+                                                                  nullptr, 0, 0);
+      tk = ko;
+      tv = vo;
+    }
+  }
+  if ((s = check_cuda(ctx, cudaGetLastError(), "tile sort")) != GSR_OK) return s;
+
+  // ---- optional O2 emission-order list ----
+  if (keys_unsorted) {
+    k_emit_o2<<<(unsigned)((M + 255) / 256), 256, 0, st>>>(p_depth, p_xr, p_yr, p_nt, (const uint32_t*)eo, M, n, gx,
+                                                           (uint32_t)tpv, keys_unsorted, vals_unsorted);
+    if ((s = check_cuda(ctx, cudaGetLastError(), "emit_o2")) != GSR_OK) return s;
+  }
+  return GSR_OK;
+}

@@ -1,0 +1,91 @@
+// gsr_internal.cuh -- shared declarations of libgsr (CUDA, sm_100a).
+//
+// Nothing here is shared with the CPU oracle (oracle/): the two implement the
+// readings of DESIGN.md independently.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cuda_fp16.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "../../include/gsr.h"
+
+namespace gsr {
+
+// ---- rasterizer constants (float32 hex in comments) ----
+constexpr float kDilation = 0.3f;          // 0x3e99999a  EWA low-pass, px^2
+constexpr float kRadiusK = 3.33f;          // 0x40551eb8  >= sqrt(2 ln 255) = 3.3290
+constexpr float kAlphaMax = 0.99f;         // 0x3f7d70a4
+constexpr float kTStop = 1e-4f;            // 0x38d1b717
+constexpr uint32_t kAlphaMinBits = 0x3b808081u;  // 1/255
+constexpr int kTile = GSR_TILE;
+
+struct CamBatch {
+  gsr_camera c[GSR_MAX_VIEWS];
+};
+
+// exp(x) for x <= 0: Cody-Waite range reduction by ln2 (hi/lo), degree-7
+// Taylor polynomial in Horner form, scale by 2^k built in the exponent field.
+// Pure IEEE float ops -> bit-identical on any correctly rounding FPU.
+__device__ __forceinline__ float exp_spec(float x) {
+  if (x < -80.0f) return 0.0f;
+  const float kf = rintf(x * __int_as_float(0x3fb8aa3b));
+  float r = __fmaf_rn(kf, -__int_as_float(0x3f317200), x);
+  r = __fmaf_rn(kf, -__int_as_float(0x35bfbe8e), r);
+  float p = __int_as_float(0x39500d01);
+  p = __fmaf_rn(p, r, __int_as_float(0x3ab60b61));
+  p = __fmaf_rn(p, r, __int_as_float(0x3c088889));
+  p = __fmaf_rn(p, r, __int_as_float(0x3d2aaaab));
+  p = __fmaf_rn(p, r, __int_as_float(0x3e2aaaab));
+  p = __fmaf_rn(p, r, __int_as_float(0x3f000000));
+  p = __fmaf_rn(p, r, 1.0f);
+  p = __fmaf_rn(p, r, 1.0f);
+  const int k = (int)kf;
+  return p * __int_as_float((k + 127) << 23);
+}
+
+// ---- context scratch ----
+enum Slot {
+  S_DKEY_A, S_DKEY_B, S_DVAL_A, S_DVAL_B,   // depth pre-sort (visible (view,g) pairs)
+  S_TKEY_A, S_TKEY_B, S_TVAL_A,             // tile sort keys / payload ping-pong
+  S_COUNTS,                                 // per (view,tile) key counts
+  S_HIST,                                   // per-pass digit histograms + bases
+  S_LOOKBACK,                               // decoupled look-back words
+  S_EMITOFF,                                // emission offsets (parity output only)
+  S_TOTALS,                                 // device totals (Nvis, K)
+  S_SORTK, S_SORTV,                         // utility sort ping-pong
+  S_SELECT,                                 // exclusion mask staging
+  S_NSLOTS
+};
+
+}  // namespace gsr
+
+struct gsr_ctx {
+  int device = 0;
+  std::string err;
+  void* buf[gsr::S_NSLOTS] = {};
+  size_t cap[gsr::S_NSLOTS] = {};
+  void* host_pinned = nullptr;  // 4 KB pinned readback area
+  int num_sms = 148;
+};
+
+namespace gsr {
+
+gsr_status set_err(gsr_ctx* ctx, gsr_status st, const std::string& msg);
+gsr_status check_cuda(gsr_ctx* ctx, cudaError_t e, const char* what);
+gsr_status ensure(gsr_ctx* ctx, Slot s, size_t bytes, void** out);
+
+// ---- launchers (each returns cudaGetLastError() of its launches) ----
+cudaError_t launch_project(const gsr_gaussians& G, const CamBatch& cams, int V, float* rec,
+                           uint32_t* bin, cudaStream_t st);
+
+// onesweep radix sort pieces (binsort.cu)
+struct SortBufs {
+  uint32_t* hist;      // [passes][256] histograms, then [passes][256] exclusive bases
+  uint32_t* lookback;  // [passes][nblocks][256]
+  uint32_t* counters;  // [passes] dynamic block ids
+};
+
+}  // namespace gsr

@@ -1,0 +1,221 @@
+// project.cu -- K1: projection + culling + SH colour for a batch of views.
+//
+// DESIGN.md O1 (projection, EWA with 0.3 px^2 dilation and 1.3x FOV clamp),
+// O4 (SH colour), O2's depth bits.  One thread per Gaussian; the batch's
+// cameras travel as a __grid_constant__ kernel parameter and the thread loops
+// over them, so the 15 float4 parameter planes (240 B at degree 3) are read
+// from HBM ONCE per batch and the view-independent 3D covariance is computed
+// once per Gaussian.  Reads/writes are coalesced float4 / uint32 planes.
+//
+// Arithmetic: float32, no contraction (-fmad=false), IEEE div/sqrt, evaluated
+// in the order DESIGN.md writes -- the bin records are bit-exact against the
+// oracle.
+#include "gsr_internal.cuh"
+
+namespace gsr {
+namespace {
+
+constexpr float SH_C1 = 0.4886025119f;
+constexpr float SH_C2a = 1.0925484306f;
+constexpr float SH_C2b = 0.3153915653f;
+constexpr float SH_C2c = 0.5462742153f;
+constexpr float SH_C3a = 0.5900435899f;
+constexpr float SH_C3b = 2.8906114426f;
+constexpr float SH_C3c = 0.4570457995f;
+constexpr float SH_C3d = 0.3731763326f;
+constexpr float SH_C3e = 1.4453057213f;
+
+template <int DEG>
+struct ShCoef {
+  static constexpr int kCoef = (DEG + 1) * (DEG + 1);
+  static constexpr int kPlanes = (3 * kCoef + 3) / 4;
+  float k[kPlanes * 4];
+};
+
+// rgb_ch = max(0, ((k0 + Y1 k1) + Y2 k2) + ...), Y0 = 1 (DC is the colour).
+template <int DEG>
+__device__ __forceinline__ void sh_colour(const ShCoef<DEG>& S, float x, float y, float z, float rgb[3]) {
+  float Y[16];
+  Y[0] = 1.0f;
+  if (DEG >= 1) {
+    Y[1] = -SH_C1 * y;
+    Y[2] = SH_C1 * z;
+    Y[3] = -SH_C1 * x;
+  }
+  if (DEG >= 2) {
+    const float xx = x * x, yy = y * y, zz = z * z;
+    const float xy = x * y, yz = y * z, xz = x * z;
+    Y[4] = SH_C2a * xy;
+    Y[5] = -SH_C2a * yz;
+    Y[6] = SH_C2b * (((2.0f * zz) - xx) - yy);
+    Y[7] = -SH_C2a * xz;
+    Y[8] = SH_C2c * (xx - yy);
+    if (DEG >= 3) {
+      Y[9] = (-SH_C3a * y) * ((3.0f * xx) - yy);
+      Y[10] = (SH_C3b * xy) * z;
+      Y[11] = (-SH_C3c * y) * (((4.0f * zz) - xx) - yy);
+      Y[12] = (SH_C3d * z) * (((2.0f * zz) - (3.0f * xx)) - (3.0f * yy));
+      Y[13] = (-SH_C3c * x) * (((4.0f * zz) - xx) - yy);
+      Y[14] = (SH_C3e * z) * (xx - yy);
+      Y[15] = (-SH_C3a * x) * (xx - (3.0f * yy));
+    }
+  }
+#pragma unroll
+  for (int ch = 0; ch < 3; ++ch) {
+    float acc = S.k[ch];
+#pragma unroll
+    for (int c = 1; c < ShCoef<DEG>::kCoef; ++c) acc = acc + Y[c] * S.k[3 * c + ch];
+    rgb[ch] = fmaxf(0.0f, acc);
+  }
+}
+
+__device__ __forceinline__ float clampf(float v, float lo, float hi) { return fminf(fmaxf(v, lo), hi); }
+
+template <int DEG>
+__global__ void __launch_bounds__(256) k1_project(const float4* __restrict__ po, const float4* __restrict__ su,
+                                                  const float4* __restrict__ rq, const float4* __restrict__ sh,
+                                                  int64_t n, int V, int gx, int gy,
+                                                  const __grid_constant__ CamBatch cams,
+                                                  float4* __restrict__ rec, uint32_t* __restrict__ bin) {
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= n) return;
+  const float4 P = __ldg(po + g);
+  const float4 Sd = __ldg(su + g);
+  const float4 Q4 = __ldg(rq + g);
+  ShCoef<DEG> S;
+#pragma unroll
+  for (int j = 0; j < ShCoef<DEG>::kPlanes; ++j) {
+    const float4 c = __ldg(sh + (int64_t)j * n + g);
+    S.k[4 * j + 0] = c.x; S.k[4 * j + 1] = c.y; S.k[4 * j + 2] = c.z; S.k[4 * j + 3] = c.w;
+  }
+  const float mx = P.x, my = P.y, mz = P.z, o = P.w;
+
+  // view-independent 3D covariance (O1 steps 4-7)
+  const float qn = sqrtf(((Q4.x * Q4.x + Q4.y * Q4.y) + Q4.z * Q4.z) + Q4.w * Q4.w);
+  const float w = Q4.x / qn, x = Q4.y / qn, y = Q4.z / qn, z = Q4.w / qn;
+  float rm[3][3];
+  rm[0][0] = 1.0f - 2.0f * (y * y + z * z);
+  rm[0][1] = 2.0f * (x * y - w * z);
+  rm[0][2] = 2.0f * (x * z + w * y);
+  rm[1][0] = 2.0f * (x * y + w * z);
+  rm[1][1] = 1.0f - 2.0f * (x * x + z * z);
+  rm[1][2] = 2.0f * (y * z - w * x);
+  rm[2][0] = 2.0f * (x * z - w * y);
+  rm[2][1] = 2.0f * (y * z + w * x);
+  rm[2][2] = 1.0f - 2.0f * (x * x + y * y);
+  const float s3[3] = {Sd.x, Sd.y, Sd.z};
+  float M[3][3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) M[i][j] = rm[i][j] * s3[j];
+  float Sg[3][3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) Sg[i][j] = (M[i][0] * M[j][0] + M[i][1] * M[j][1]) + M[i][2] * M[j][2];
+
+  // alpha-skip bound (GPU-only shortcut, exact semantics): power < tau implies
+  // o * exp(power) < 1/255 with a 1e-3 margin far above exp_spec's 1.1e-7 error.
+  const float tau = -logf(255.0f * o) - 1e-3f;
+  const float thr = 2.0f * logf(255.0f * o) + 2e-3f;  // q threshold of the alpha >= 1/255 region
+
+  const int64_t VN = (int64_t)V * n;
+  for (int c = 0; c < V; ++c) {
+    const gsr_camera& cam = cams.c[c];
+    const float* R = cam.R;
+    const int64_t cg = (int64_t)c * n + g;
+    uint32_t depth = 0, xr = 0, yr = 0, nt = 0;
+    const float vx = ((R[0] * mx + R[1] * my) + R[2] * mz) + cam.t[0];
+    const float vy = ((R[3] * mx + R[4] * my) + R[5] * mz) + cam.t[1];
+    const float vz = ((R[6] * mx + R[7] * my) + R[8] * mz) + cam.t[2];
+    if (vz > cam.znear) {
+      const float xn = vx / vz, yn = vy / vz;
+      const float u = cam.fx * xn + cam.cx;
+      const float v = cam.fy * yn + cam.cy;
+      const float tx = fminf(cam.limx, fmaxf(-cam.limx, xn)) * vz;
+      const float ty = fminf(cam.limy, fmaxf(-cam.limy, yn)) * vz;
+      const float j00 = cam.fx / vz, j11 = cam.fy / vz, z2 = vz * vz;
+      const float j02 = -(cam.fx * tx) / z2;
+      const float j12 = -(cam.fy * ty) / z2;
+      float T[2][3];
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        T[0][k] = j00 * R[k] + j02 * R[6 + k];
+        T[1][k] = j11 * R[3 + k] + j12 * R[6 + k];
+      }
+      float Qm[2][3];
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int k = 0; k < 3; ++k) Qm[i][k] = (T[i][0] * Sg[0][k] + T[i][1] * Sg[1][k]) + T[i][2] * Sg[2][k];
+      const float a = ((Qm[0][0] * T[0][0] + Qm[0][1] * T[0][1]) + Qm[0][2] * T[0][2]) + kDilation;
+      const float b = (Qm[0][0] * T[1][0] + Qm[0][1] * T[1][1]) + Qm[0][2] * T[1][2];
+      const float cc = ((Qm[1][0] * T[1][0] + Qm[1][1] * T[1][1]) + Qm[1][2] * T[1][2]) + kDilation;
+      const float det = a * cc - b * b;
+      if (det > 0.0f) {
+        const float mid = 0.5f * (a + cc);
+        const float lam = mid + sqrtf(fmaxf(mid * mid - det, 0.0f));
+        const float r = ceilf(kRadiusK * sqrtf(lam));
+        const uint32_t x0 = (uint32_t)clampf(floorf((u - r) * 0.0625f), 0.0f, (float)gx);
+        const uint32_t x1 = (uint32_t)clampf(ceilf((u + r) * 0.0625f), 0.0f, (float)gx);
+        const uint32_t y0 = (uint32_t)clampf(floorf((v - r) * 0.0625f), 0.0f, (float)gy);
+        const uint32_t y1 = (uint32_t)clampf(ceilf((v + r) * 0.0625f), 0.0f, (float)gy);
+        const uint32_t ntt = (x1 - x0) * (y1 - y0);
+        if (ntt > 0) {
+          depth = __float_as_uint(vz);
+          xr = x0 | (x1 << 16);
+          yr = y0 | (y1 << 16);
+          nt = ntt;
+          const float inv = 1.0f / det;
+          const float A = cc * inv, B = -(b * inv), C = a * inv;
+          // SH colour
+          const float dx = mx - cam.campos[0], dy = my - cam.campos[1], dz = mz - cam.campos[2];
+          const float len = sqrtf((dx * dx + dy * dy) + dz * dz);
+          float rgb[3];
+          sh_colour<DEG>(S, dx / len, dy / len, dz / len, rgb);
+          // conservative half-extents of {q <= thr}: sqrt(thr * Sigma'_xx), rounded up to fp16
+          float ex = 0.0f, ey = 0.0f;
+          if (thr > 0.0f) {
+            ex = fminf(sqrtf(thr * a) * 1.001f + 0.05f, 65504.0f);
+            ey = fminf(sqrtf(thr * cc) * 1.001f + 0.05f, 65504.0f);
+          }
+          const uint32_t ext = (uint32_t)__half_as_ushort(__float2half_ru(ex)) |
+                               ((uint32_t)__half_as_ushort(__float2half_ru(ey)) << 16);
+          float4* rr = rec + cg * 3;
+          rr[0] = make_float4(u, v, A, B);
+          rr[1] = make_float4(C, o, Sd.w, tau);
+          rr[2] = make_float4(rgb[0], rgb[1], rgb[2], __uint_as_float(ext));
+        }
+      }
+    }
+    bin[cg] = depth;
+    bin[VN + cg] = xr;
+    bin[2 * VN + cg] = yr;
+    bin[3 * VN + cg] = nt;
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_project(const gsr_gaussians& G, const CamBatch& cams, int V, float* rec, uint32_t* bin,
+                           cudaStream_t st) {
+  const int W = cams.c[0].width, H = cams.c[0].height;
+  const int gx = (W + kTile - 1) / kTile, gy = (H + kTile - 1) / kTile;
+  const int64_t n = G.n;
+  const unsigned blocks = (unsigned)((n + 255) / 256);
+  auto po = reinterpret_cast<const float4*>(G.pos_opacity);
+  auto su = reinterpret_cast<const float4*>(G.scale_unc);
+  auto rq = reinterpret_cast<const float4*>(G.rot);
+  auto sh = reinterpret_cast<const float4*>(G.sh);
+  auto r4 = reinterpret_cast<float4*>(rec);
+  switch (G.sh_degree) {
+    case 0: k1_project<0><<<blocks, 256, 0, st>>>(po, su, rq, sh, n, V, gx, gy, cams, r4, bin); break;
+    case 1: k1_project<1><<<blocks, 256, 0, st>>>(po, su, rq, sh, n, V, gx, gy, cams, r4, bin); break;
+    case 2: k1_project<2><<<blocks, 256, 0, st>>>(po, su, rq, sh, n, V, gx, gy, cams, r4, bin); break;
+    default: k1_project<3><<<blocks, 256, 0, st>>>(po, su, rq, sh, n, V, gx, gy, cams, r4, bin); break;
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace gsr

@@ -1,0 +1,209 @@
+"""Thin ctypes binding of libgsr (include/gsr.h): argument marshalling only.
+
+Every step of the hot path runs in the CUDA kernels of ``csrc/``; this module
+turns torch CUDA tensors / numpy camera arrays into the C-ABI's plain
+pointers and raises ``GsrError`` on a non-OK status.  There is no CPU
+fallback: if ``libgsr.so`` is missing the import fails loudly.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Optional
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libgsr.so")
+
+GSR_OK, GSR_EINVAL, GSR_ECUDA, GSR_ENOMEM, GSR_ECAPACITY, GSR_EBUDGET = range(6)
+STATUS_NAMES = {0: "GSR_OK", 1: "GSR_EINVAL", 2: "GSR_ECUDA", 3: "GSR_ENOMEM", 4: "GSR_ECAPACITY",
+                5: "GSR_EBUDGET"}
+GSR_MAX_VIEWS = 64
+GSR_TILE = 16
+
+# gsr_camera (96 bytes), field for field
+CAM_DTYPE = np.dtype(
+    [("R", "<f4", (9,)), ("t", "<f4", (3,)), ("campos", "<f4", (3,)), ("fx", "<f4"), ("fy", "<f4"),
+     ("cx", "<f4"), ("cy", "<f4"), ("limx", "<f4"), ("limy", "<f4"), ("znear", "<f4"),
+     ("width", "<i4"), ("height", "<i4")], align=True)
+assert CAM_DTYPE.itemsize == 96
+
+EXPORTED = ["gsr_create", "gsr_destroy", "gsr_last_error", "gsr_version", "gsr_camera_look_at",
+            "gsr_project", "gsr_bin_sort", "gsr_composite", "gsr_score_views", "gsr_select_nbv",
+            "gsr_sort_pairs_u64", "gsr_scratch_bytes"]
+
+
+class GsrError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS_NAMES.get(status, status)}: {msg}")
+        self.status = status
+
+
+class _Gaussians(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int64), ("sh_degree", ctypes.c_int32), ("reserved", ctypes.c_int32),
+                ("pos_opacity", ctypes.c_void_p), ("scale_unc", ctypes.c_void_p), ("rot", ctypes.c_void_p),
+                ("sh", ctypes.c_void_p)]
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"libgsr.so not built at {LIB_PATH}: run `python -c 'import __graft_entry__ as g; "
+                          f"g.build()'` (nvcc, sm_100a). There is no CPU fallback.")
+    L = ctypes.CDLL(LIB_PATH)
+    P, i64, i32, st = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_int
+    L.gsr_create.argtypes = [ctypes.POINTER(P), ctypes.c_int]
+    L.gsr_destroy.argtypes = [P]
+    L.gsr_last_error.argtypes = [P]
+    L.gsr_last_error.restype = ctypes.c_char_p
+    L.gsr_version.restype = ctypes.c_char_p
+    L.gsr_camera_look_at.argtypes = [ctypes.c_double] * 3 + [P, i32, i32, ctypes.c_double, ctypes.c_double, P]
+    L.gsr_project.argtypes = [P, P, P, i32, P, P, P]
+    L.gsr_bin_sort.argtypes = [P, P, i64, P, i32, P, P, i64, P, P, P, P, P]
+    L.gsr_composite.argtypes = [P, P, i64, P, P, P, i32, P, P, P, P, P, P]
+    L.gsr_score_views.argtypes = [P, P, P, i32, P, P]
+    L.gsr_select_nbv.argtypes = [P, P, i32, P, i32, P, P]
+    L.gsr_sort_pairs_u64.argtypes = [P, P, P, P, P, i64, i32, i32, P]
+    L.gsr_scratch_bytes.argtypes = [P]
+    L.gsr_scratch_bytes.restype = i64
+    for name in EXPORTED:
+        if name not in ("gsr_last_error", "gsr_version", "gsr_scratch_bytes"):
+            getattr(L, name).restype = st
+    return L
+
+
+lib = _load()
+
+
+def version() -> str:
+    return lib.gsr_version().decode()
+
+
+def _ptr(t) -> Optional[int]:
+    if t is None:
+        return None
+    if isinstance(t, np.ndarray):
+        return t.ctypes.data
+    return t.data_ptr()
+
+
+def _stream(stream) -> Optional[int]:
+    if stream is None:
+        import torch
+        return torch.cuda.current_stream().cuda_stream
+    if isinstance(stream, int):
+        return stream
+    return stream.cuda_stream
+
+
+def cams_array(cams) -> np.ndarray:
+    a = np.ascontiguousarray(np.asarray(cams).reshape(-1))
+    if a.dtype != CAM_DTYPE:
+        a = a.astype(CAM_DTYPE)
+    return a
+
+
+def gsr_camera_look_at(elevation: float, azimuth: float, radius: float, target, width: int, height: int,
+                       focal: float, znear: float = 0.2) -> np.ndarray:
+    """H1: θ = (elevation, azimuth, radius) -> one camera struct."""
+    out = np.zeros(1, dtype=CAM_DTYPE)
+    tgt = np.ascontiguousarray(np.asarray(target, dtype=np.float64).reshape(3))
+    st = lib.gsr_camera_look_at(elevation, azimuth, radius, tgt.ctypes.data, width, height, focal, znear,
+                                out.ctypes.data)
+    if st != GSR_OK:
+        raise GsrError(st, lib.gsr_last_error(None).decode())
+    return out[0]
+
+
+class Gaussians:
+    """Device-resident packed field: planes[P][n][4] float32 CUDA tensor."""
+
+    def __init__(self, planes, sh_degree: int):
+        assert planes.is_cuda and planes.dtype.is_floating_point and planes.shape[-1] == 4
+        self.planes = planes.contiguous()
+        self.sh_degree = int(sh_degree)
+        self.n = int(planes.shape[1])
+
+    def struct(self) -> _Gaussians:
+        base = self.planes.data_ptr()
+        stride = self.n * 16
+        return _Gaussians(self.n, self.sh_degree, 0, base, base + stride, base + 2 * stride, base + 3 * stride)
+
+
+class Context:
+    """A gsr_ctx (scratch owner) bound to one device; one per stream/thread."""
+
+    def __init__(self, device: int = 0):
+        h = ctypes.c_void_p()
+        st = lib.gsr_create(ctypes.byref(h), device)
+        if st != GSR_OK:
+            raise GsrError(st, lib.gsr_last_error(None).decode())
+        self.handle = h
+        self.device = device
+
+    def close(self):
+        if self.handle:
+            lib.gsr_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _check(self, st: int):
+        if st != GSR_OK:
+            raise GsrError(st, lib.gsr_last_error(self.handle).decode())
+
+    def scratch_bytes(self) -> int:
+        return int(lib.gsr_scratch_bytes(self.handle))
+
+
+def gsr_project(ctx: Context, g: Gaussians, cams, render_rec, bin_rec, stream=None):
+    c = cams_array(cams)
+    gs = g.struct()
+    ctx._check(lib.gsr_project(ctx.handle, ctypes.byref(gs), c.ctypes.data, len(c), _ptr(render_rec),
+                               _ptr(bin_rec), _stream(stream)))
+
+
+def gsr_bin_sort(ctx: Context, bin_rec, n: int, cams, vals, capacity: int, ranges, keys=None,
+                 keys_unsorted=None, vals_unsorted=None, stream=None) -> int:
+    """Returns K (SYNC readback).  Raises GsrError(GSR_ECAPACITY) with .required = K."""
+    c = cams_array(cams)
+    nk = ctypes.c_int64(0)
+    st = lib.gsr_bin_sort(ctx.handle, _ptr(bin_rec), n, c.ctypes.data, len(c), _ptr(keys), _ptr(vals), capacity,
+                          ctypes.byref(nk), _ptr(ranges), _ptr(keys_unsorted), _ptr(vals_unsorted),
+                          _stream(stream))
+    if st == GSR_ECAPACITY:
+        e = GsrError(st, lib.gsr_last_error(ctx.handle).decode())
+        e.required = int(nk.value)
+        raise e
+    ctx._check(st)
+    return int(nk.value)
+
+
+def gsr_composite(ctx: Context, render_rec, n: int, vals, ranges, cams, tile_partial, rgbu=None, t_final=None,
+                  n_contrib=None, n_frag=None, stream=None):
+    c = cams_array(cams)
+    ctx._check(lib.gsr_composite(ctx.handle, _ptr(render_rec), n, _ptr(vals), _ptr(ranges), c.ctypes.data, len(c),
+                                 _ptr(rgbu), _ptr(t_final), _ptr(n_contrib), _ptr(tile_partial), _ptr(n_frag),
+                                 _stream(stream)))
+
+
+def gsr_score_views(ctx: Context, tile_partial, cams, scores, stream=None):
+    c = cams_array(cams)
+    ctx._check(lib.gsr_score_views(ctx.handle, _ptr(tile_partial), c.ctypes.data, len(c), _ptr(scores),
+                                   _stream(stream)))
+
+
+def gsr_select_nbv(ctx: Context, scores, k: int, out_idx, exclude: Optional[np.ndarray] = None, stream=None):
+    ex = None if exclude is None else np.ascontiguousarray(np.asarray(exclude, dtype=np.uint8))
+    ctx._check(lib.gsr_select_nbv(ctx.handle, _ptr(scores), int(scores.numel()), _ptr(ex), k, _ptr(out_idx),
+                                  _stream(stream)))
+
+
+def gsr_sort_pairs_u64(ctx: Context, keys_in, vals_in, keys_out, vals_out, begin_bit: int = 0, end_bit: int = 64,
+                       stream=None):
+    ctx._check(lib.gsr_sort_pairs_u64(ctx.handle, _ptr(keys_in), _ptr(vals_in), _ptr(keys_out), _ptr(vals_out),
+                                      int(keys_in.numel()), begin_bit, end_bit, _stream(stream)))

@@ -1,0 +1,96 @@
+"""Run the CUDA path through the C ABI and bring every output back to numpy."""
+import numpy as np
+import torch
+
+import oracle
+
+
+def to_dev(field):
+    from paper_2602_15355_b200 import Gaussians
+    return Gaussians(torch.from_numpy(np.ascontiguousarray(field.planes)).cuda(), field.sh_degree)
+
+
+def gpu_batch(ctx, field, cams, images=True, want_unsorted=True, want_keys=True):
+    """One batch (len(cams) <= 64, same W,H) through K1..K7; numpy outputs."""
+    from paper_2602_15355_b200 import gsr
+    G = to_dev(field)
+    V, n = len(cams), field.n
+    W, H = int(cams[0]["width"]), int(cams[0]["height"])
+    gx, gy = (W + 15) // 16, (H + 15) // 16
+    T = V * gx * gy
+    rec = torch.full((V, max(n, 1), 12), float("nan"), dtype=torch.float32, device="cuda")
+    binr = torch.full((4, V, max(n, 1)), -1, dtype=torch.int32, device="cuda")
+    gsr.gsr_project(ctx, G, cams, rec, binr)
+    cap = 0
+    vals = torch.empty(1, dtype=torch.int32, device="cuda")
+    ranges = torch.full((T, 2), -1, dtype=torch.int32, device="cuda")
+    try:
+        gsr.gsr_bin_sort(ctx, binr, n, cams, vals, 0, ranges)
+        K = 0
+    except gsr.GsrError as e:
+        assert e.status == gsr.GSR_ECAPACITY
+        K = e.required
+    cap = max(K, 1)
+    vals = torch.full((cap,), -1, dtype=torch.int32, device="cuda")
+    keys = torch.full((cap,), -1, dtype=torch.int64, device="cuda") if want_keys else None
+    ku = torch.full((cap,), -1, dtype=torch.int64, device="cuda") if want_unsorted else None
+    vu = torch.full((cap,), -1, dtype=torch.int32, device="cuda") if want_unsorted else None
+    K2 = gsr.gsr_bin_sort(ctx, binr, n, cams, vals, cap, ranges, keys=keys, keys_unsorted=ku, vals_unsorted=vu)
+    assert K2 == K
+    partial = torch.full((T,), float("nan"), dtype=torch.float32, device="cuda")
+    rgbu = torch.full((V, H, W, 4), float("nan"), dtype=torch.float32, device="cuda") if images else None
+    tf = torch.full((V, H, W), float("nan"), dtype=torch.float32, device="cuda") if images else None
+    nc = torch.full((V, H, W), -1, dtype=torch.int32, device="cuda") if images else None
+    nfrag = torch.zeros(1, dtype=torch.int64, device="cuda")
+    gsr.gsr_composite(ctx, rec, n, vals, ranges, cams, partial, rgbu=rgbu, t_final=tf, n_contrib=nc, n_frag=nfrag)
+    scores = torch.full((V,), float("nan"), dtype=torch.float32, device="cuda")
+    gsr.gsr_score_views(ctx, partial, cams, scores)
+    torch.cuda.synchronize()
+    out = dict(K=K, rec=rec.cpu().numpy(), bin=binr.cpu().numpy().view(np.uint32),
+               vals=vals.cpu().numpy().view(np.uint32)[:K], ranges=ranges.cpu().numpy().view(np.uint32),
+               partial=partial.cpu().numpy(), scores=scores.cpu().numpy(), n_frag=int(nfrag.item()))
+    if want_keys:
+        out["keys"] = keys.cpu().numpy().view(np.uint64)[:K]
+    if want_unsorted:
+        out["keys_unsorted"] = ku.cpu().numpy().view(np.uint64)[:K]
+        out["vals_unsorted"] = vu.cpu().numpy().view(np.uint32)[:K]
+    if images:
+        out.update(rgbu=rgbu.cpu().numpy(), t_final=tf.cpu().numpy(), n_contrib=nc.cpu().numpy().view(np.uint32))
+    return out
+
+
+def oracle_batch(field, cams, images=True):
+    """The oracle's expected outputs for the same batch."""
+    projs = [oracle.project(field, c) for c in cams]
+    bs = oracle.bin_sort_batch(projs, cams)
+    gx, gy = oracle.grid(cams[0])
+    tpv = gx * gy
+    res = dict(projs=projs, **bs)
+    if images:
+        imgs, tfs, ncs, scores, nfrag = [], [], [], [], 0
+        for v, (p, c) in enumerate(zip(projs, cams)):
+            rv = bs["ranges"][v * tpv:(v + 1) * tpv]
+            o = oracle.composite_tiled(p, bs["vals"], rv, c)
+            imgs.append(o["rgbu"])
+            tfs.append(o["t_final"])
+            ncs.append(o["n_contrib"])
+            scores.append(o["score"])
+            nfrag += o["n_frag"]
+        res.update(rgbu=np.stack(imgs), t_final=np.stack(tfs), n_contrib=np.stack(ncs),
+                   scores=np.array(scores), n_frag=nfrag)
+    return res
+
+
+def check_projection(gpu, orc, n):
+    """Bin records bit-exact; render records bit-exact where visible."""
+    for v, p in enumerate(orc["projs"]):
+        b = gpu["bin"][:, v, :n]
+        assert np.array_equal(b[3], p["n_tiles"]), f"view {v}: n_tiles"
+        assert np.array_equal(b[0], p["depth_bits"]), f"view {v}: depth"
+        assert np.array_equal(b[1] & 0xFFFF, p["x0"]) and np.array_equal(b[1] >> 16, p["x1"])
+        assert np.array_equal(b[2] & 0xFFFF, p["y0"]) and np.array_equal(b[2] >> 16, p["y1"])
+        vis = p["n_tiles"] > 0
+        r = gpu["rec"][v, :n][vis]
+        for col, name in [(0, "u"), (1, "v"), (2, "A"), (3, "B"), (4, "C"), (5, "o"), (6, "unc"),
+                          (8, "r"), (9, "g"), (10, "b")]:
+            assert np.array_equal(r[:, col].view(np.uint32), p[name][vis].view(np.uint32)), f"view {v}: {name}"
