@@ -41,20 +41,21 @@ def needs_build() -> bool:
     return any(os.path.getmtime(d) > t for d in deps())
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not needs_build():
+def build(force: bool = False, verbose: bool = False, debug: bool = False) -> str:
+    lib = LIB.replace("libgsr.so", "libgsr_debug.so") if debug else LIB
+    if not force and not debug and not needs_build():
         return LIB
-    tmp = LIB + ".tmp"
-    cmd = [NVCC, *NVCC_FLAGS, "-shared", "-o", tmp, *sources(),
+    tmp = lib + ".tmp"
+    extra = ["-DGSR_DEBUG"] if debug else []
+    cmd = [NVCC, *NVCC_FLAGS, *extra, "-shared", "-o", tmp, *sources(),
            "-Xlinker", "--version-script=" + os.path.join(CSRC, "exports.map")]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd), file=sys.stderr)
     subprocess.check_call(cmd)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose="-v" in sys.argv)
-    print(LIB)
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, debug="--debug" in sys.argv))

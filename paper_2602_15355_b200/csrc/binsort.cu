@@ -37,6 +37,27 @@ constexpr uint32_t DG_AGG = 1u << 30, DG_INC = 2u << 30, DG_VAL = (1u << 30) - 1
 
 __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31; }
 
+// Look-back words are read and written with volatile relaxed gpu-scope
+// accesses: the flag and the count share one word, so no fence is needed, but
+// the loads MUST be volatile -- with a plain (CSE-able) load the compiler may
+// assume a spin on an unchanged word never happens and fold it away.
+__device__ __forceinline__ uint32_t ld_word(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint64_t ld_word(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_word(uint32_t* p, uint32_t v) {
+  asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void st_word(uint64_t* p, uint64_t v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
 template <typename T>
 __device__ __forceinline__ T warp_incl_scan(T v) {
 #pragma unroll
@@ -62,7 +83,7 @@ __device__ uint64_t warp_lookback(const uint64_t* words, int64_t bid) {
   int64_t base = bid - 1;
   while (true) {
     const int64_t idx = base - lane;
-    uint64_t w = idx >= 0 ? __ldcv((const unsigned long long*)words + idx) : LB_INC;
+    uint64_t w = idx >= 0 ? ld_word(words + idx) : LB_INC;
     const uint32_t f = (uint32_t)(w >> 62);
     const uint32_t notready = __ballot_sync(FULL, f == 0);
     const uint32_t inc = __ballot_sync(FULL, f == 2);
@@ -82,7 +103,7 @@ __device__ uint64_t warp_lookback(const uint64_t* words, int64_t bid) {
 }
 
 __device__ __forceinline__ void publish(uint64_t* words, int64_t bid, uint64_t v) {
-  __stcg((unsigned long long*)words + bid, (unsigned long long)v);
+  st_word(words + bid, v);
 }
 
 // ---------------------------------------------------------------------------
@@ -276,19 +297,25 @@ __global__ void __launch_bounds__(256) onesweep(const KeyT* __restrict__ kin, co
     uint32_t* my = lookback + (size_t)bid * 256 + d;
     uint32_t excl = 0;
     if (bid == 0) {
-      __stcg(my, DG_INC | total);
+      st_word(my, DG_INC | total);
     } else {
-      __stcg(my, DG_AGG | total);
+      st_word(my, DG_AGG | total);
       int64_t j = (int64_t)bid - 1;
       while (true) {
-        const uint32_t w = __ldcv(lookback + (size_t)j * 256 + d);
+#ifdef GSR_DEBUG
+        if (j < 0) {
+          printf("onesweep lookback underflow bid=%u d=%d n=%u shift=%d\n", bid, d, n, shift);
+          __trap();
+        }
+#endif
+        const uint32_t w = ld_word(lookback + (size_t)j * 256 + d);
         const uint32_t f = w >> 30;
         if (f == 0) continue;
         excl += w & DG_VAL;
         if (f == 2) break;
         --j;
       }
-      __stcg(my, DG_INC | (excl + total));
+      st_word(my, DG_INC | (excl + total));
     }
     // block-local exclusive scan of totals over digits
     const uint32_t inc = warp_incl_scan<uint32_t>(total);
@@ -325,6 +352,12 @@ __global__ void __launch_bounds__(256) onesweep(const KeyT* __restrict__ kin, co
     const uint32_t vv = u.st.v[i];
     const uint32_t d = (uint32_t)(kk >> shift) & mask;
     const uint32_t o = s_gbase[d] + i;
+#ifdef GSR_DEBUG
+    if (o >= n) {
+      printf("onesweep OOB write bid=%u d=%u i=%d o=%u n=%u base=%u start=%u\n", bid, d, i, o, n, base[d], s_start[d]);
+      __trap();
+    }
+#endif
     if (MODE == 0) {
       kout[o] = kk;
       vout[o] = vv;

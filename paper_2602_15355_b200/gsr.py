@@ -14,7 +14,7 @@ from typing import Optional
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libgsr.so")
+LIB_PATH = os.environ.get("GSR_LIB") or os.path.join(_HERE, "libgsr.so")
 
 GSR_OK, GSR_EINVAL, GSR_ECUDA, GSR_ENOMEM, GSR_ECAPACITY, GSR_EBUDGET = range(6)
 STATUS_NAMES = {0: "GSR_OK", 1: "GSR_EINVAL", 2: "GSR_ECUDA", 3: "GSR_ENOMEM", 4: "GSR_ECAPACITY",
