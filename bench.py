@@ -1,0 +1,303 @@
+#!/usr/bin/env python
+"""bench.py -- candidate views scored / s (+ fragments / s, roofline) for the
+active-view scoring hot path of DAV-GSWT (arXiv 2602.15355) on B200.
+
+Workload (BASELINE.json configs[2], the configuration the metric's target is
+quoted on; fits one GPU): 1,000,000 Gaussians (SH degree 3), 1,024 candidate
+cameras on a Fibonacci hemisphere of radius 4, 800x800 px, f = 900 px.
+One step = one Alg. 1 scoring iteration: [N>1: broadcast
+of the field] -> every candidate view projected, binned, sorted, composited
+and scored (views sharded v mod N over ranks) -> [N>1: all-gather of the
+scores] -> NBV selection.  Strong scaling: the 1,024 views are split over N.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl gsr|reference]
+
+N > 1 is launched by torchrun (one rank per GPU, NCCL).  Rank 0 prints ONE
+JSON line.  `--impl reference` times the CPU oracle (the reference arm of
+this tier) on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "candidate_views_scored_per_sec"
+UNIT = "views/s"
+CONFIG_ID = 3
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="gsr", choices=["gsr", "reference"])
+    p.add_argument("--batch-views", type=int, default=16)
+    p.add_argument("--cpu-views", type=int, default=0, help="oracle sample size (0 = auto)")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-e2e", action="store_true")
+    return p.parse_args()
+
+
+def load_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        d = json.load(open(path))
+        return dict(hbm_gbs=float(d["hbm_gbs"]), sm_max_mhz=float(d.get("sm_max_mhz", 1965.0)), source="measured")
+    return dict(hbm_gbs=6650.0, sm_max_mhz=1965.0, source="fallback")
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        rows = [r for r in self.rows if len(r) >= 8]
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[4 + i].lower().startswith("active")})
+        loaded = [s for s in sm if s > 0.5 * (max(sm) if sm else 1)]
+        return {"sm_mhz": float(np.median(loaded)) if loaded else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(rows)}
+
+
+# ----------------------------------------------------------------------------- reference arm
+def run_reference(args, scene, cfg_json):
+    import oracle
+    n_threads = os.cpu_count() or 1
+    nv = args.cpu_views or max(8, min(32, 2 * n_threads))
+    idx = np.linspace(0, len(scene.cameras) - 1, nv).round().astype(np.int64)
+    cams = np.ascontiguousarray(scene.cameras[idx])
+    oracle.build()
+    times = []
+    fr = 0
+    for step in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        scores, nf, nk, _ = oracle.render_views(scene.field, cams, n_threads=n_threads)
+        sel = oracle.select_topk(scores, 1)
+        dt = time.perf_counter() - t0
+        if step >= args.warmup:
+            times.append(dt)
+            fr = int(nf.sum())
+        if step == 0 and args.warmup + args.steps > 2 and dt > 60:
+            break
+    t = float(np.mean(times)) if times else float("nan")
+    v = nv / t
+    sample = (f"{nv} strided views of the 1,024 (full O1-O6 oracle per view: projection, "
+              f"duplication, qsort, tiled compositing, score) + top-1")
+    return {"metric": METRIC, "value": v, "unit": UNIT, "impl": "reference", "n_gpus": 0,
+            "steps": len(times), "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": cfg_json,
+            "fragments_per_sec": fr / t,
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": n_threads, "kind": "oracle", "sample": sample},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def cpu_baseline(scene, n_views: int):
+    import oracle
+    n_threads = os.cpu_count() or 1
+    nv = n_views or max(8, min(32, 2 * n_threads))
+    idx = np.linspace(0, len(scene.cameras) - 1, nv).round().astype(np.int64)
+    cams = np.ascontiguousarray(scene.cameras[idx])
+    oracle.build()
+    t0 = time.perf_counter()
+    scores, nf, nk, _ = oracle.render_views(scene.field, cams, n_threads=n_threads)
+    dt = time.perf_counter() - t0
+    return {"value": nv / dt, "unit": UNIT, "cores": n_threads, "kind": "oracle",
+            "sample": f"{nv} strided views of the 1,024 at 800x800 (1M Gaussians), full O1-O6 oracle, "
+                      f"{dt:.1f} s wall on {n_threads} threads", "fragments_per_sec": float(nf.sum()) / dt}
+
+
+# ----------------------------------------------------------------------------- GPU arm
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    import synth
+    cfg_json = {"workload": synth.CONFIG_NAMES[CONFIG_ID], "gaussians": 1_000_000, "sh_degree": 3,
+                "views": 1024, "width": 800, "height": 800, "focal_px": 900, "tile": 16,
+                "batch_views": args.batch_views, "parallelism": f"dp{world} (views v mod N)",
+                "l2": "inputs larger than L2: 240 MB field + ~0.9 GB keys per 16-view batch, no flush"}
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        scene = synth.make_scene(CONFIG_ID)
+        print(json.dumps(run_reference(args, scene, cfg_json)), flush=True)
+        return
+
+    import torch
+    import torch.distributed as dist
+    from paper_2602_15355_b200 import Gaussians, gsr
+    from paper_2602_15355_b200.distributed import broadcast_field, score_and_select
+    from paper_2602_15355_b200.pipeline import ViewScorer
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    scene = synth.make_scene(CONFIG_ID) if rank == 0 else synth.make_scene(CONFIG_ID, n_override=1, views=1024)
+    P = 3 + synth.n_sh_planes(3)
+    n = 1_000_000
+    host_planes = torch.empty((P, n, 4), dtype=torch.float32).pin_memory()
+    if rank == 0:
+        host_planes.copy_(torch.from_numpy(scene.field.planes))
+    cams = synth.fibonacci_cameras(1024, 4.0, 800, 800, 900.0)
+    planes = torch.empty((P, n, 4), dtype=torch.float32, device=dev)
+    planes.copy_(host_planes, non_blocking=False)
+    G = Gaussians(planes, 3)
+    scorer = ViewScorer(G, batch_views=args.batch_views)
+    ctx = scorer.ctx
+
+    def score_fn(c):
+        return scorer.score_views(c)
+
+    def select_fn(scores, k, exclude):
+        return scorer.select(scores, k, exclude)
+
+    def step(e2e: bool = False):
+        if e2e and rank == 0:
+            planes.copy_(host_planes, non_blocking=True)  # H2D of the step's inputs
+        broadcast_field(planes)
+        scores, sel = score_and_select(cams, score_fn, select_fn, 1)
+        if e2e:
+            out = torch.cat([scores, sel.float()]).cpu()  # D2H of the step's result
+            return out
+        return sel
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def timed(k, e2e=False, stage_timing=False):
+        ctx.timing(stage_timing)
+        ctx.timing_read()
+        scorer.n_frag.zero_()
+        barrier()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0 = time.perf_counter()
+        ev0.record()
+        for _ in range(k):
+            step(e2e)
+        ev1.record()
+        barrier()
+        wall = time.perf_counter() - t0
+        ms = ev0.elapsed_time(ev1)
+        stages = ctx.timing_read()
+        ctx.timing(False)
+        t = torch.tensor([ms, wall * 1e3], dtype=torch.float64, device=dev)
+        fr = scorer.n_frag.clone().to(torch.float64)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            dist.all_reduce(fr, op=dist.ReduceOp.SUM)
+        return float(t[0].item()), float(t[1].item()), fr.tolist(), stages
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    ms, wall_ms, frags, stages = timed(args.steps, stage_timing=True)
+    clk = clocks.stop()
+    ms_t, _, _, _ = (ms, None, None, None)
+    # value: whole-job views/s, device time max over ranks
+    views_per_s = 1024 * args.steps / (ms / 1e3)
+    frag_per_s = frags[0] / (ms / 1e3)
+    eval_per_s = frags[1] / (ms / 1e3)
+
+    # e2e: through the public API with the field copied H2D from pinned host
+    # memory every step and the scores + NBV read back D2H
+    e2e = None
+    if not args.no_e2e:
+        ms_e, _, _, _ = timed(args.steps, e2e=True)
+        e2e = {"value": 1024 * args.steps / (ms_e / 1e3), "unit": UNIT,
+               "h2d_bytes_per_step": int(planes.numel() * 4 + 96 * 1024),
+               "d2h_bytes_per_step": int(4 * 1024 + 4)}
+
+    peaks = load_peaks()
+    st_ms = {k: v["ms"] / args.steps for k, v in stages.items()}
+    st_by = {k: v["bytes"] / args.steps for k, v in stages.items()}
+    launches = sum(v["launches"] for v in stages.values())
+    stage_tab = {k: {"ms_per_step": round(st_ms[k], 4), "algo_GB_per_step": round(st_by[k] / 1e9, 4),
+                     "GB_per_s": round(st_by[k] / (st_ms[k] / 1e3) / 1e9, 1) if st_ms[k] > 0 else None,
+                     "launches_per_step": stages[k]["launches"] / args.steps}
+                 for k in stages if stages[k]["launches"]}
+    # roofline of the dominant HBM-bound kernel stage (largest device time among
+    # the sort / bin / projection stages) and of the composite (ALU) stage
+    hbm_stages = ["project", "compact", "depth_sort", "emit", "ranges", "tile_sort"]
+    dom = max(hbm_stages, key=lambda s: st_ms[s])
+    top = max(st_ms, key=lambda s: st_ms[s])
+    ach = st_by[dom] / (st_ms[dom] / 1e3) / 1e9
+    roof = {"bound": "hbm", "kernel": dom, "achieved": round(ach, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
+            "frac": round(ach / peaks["hbm_gbs"], 4), "traffic": None,
+            "peak_source": peaks["source"] + " hbm_gbs (MEASURED_PEAKS.json)",
+            "dominant_stage_of_step": top}
+    if top == "composite":
+        # K6 is bound by the issue rate of FP32/ALU instructions
+        f = (clk.get("sm_mhz") or peaks["sm_max_mhz"]) * 1e6
+        peak_ops = 148 * 128 * f
+        roof["composite"] = {"bound": "alu", "evaluated_pairs_per_s": eval_per_s, "fragments_per_s": frag_per_s,
+                             "ms_per_step": st_ms["composite"], "sm_clock_hz": f, "peak_lane_ops_per_s": peak_ops}
+
+    line = {"metric": METRIC, "value": round(views_per_s, 2), "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 3),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (seeded generator of BASELINE.json configs[2]; no dataset)",
+            "config": cfg_json, "fragments_per_sec": frag_per_s, "evaluated_pairs_per_sec": eval_per_s,
+            "wall_ms_per_step": round(wall_ms / args.steps, 3), "roofline": roof, "stages": stage_tab,
+            "gpu_launches": int(launches * world), "clocks": clk, "e2e": e2e,
+            "keys_per_step_rank0": int(sum(scorer.last_keys))}
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(scene, args.cpu_views)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

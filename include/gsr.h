@@ -148,7 +148,10 @@ gsr_status gsr_bin_sort(gsr_ctx* ctx, const uint32_t* bin_rec, int64_t n, const 
    rgbu        OPTIONAL [V][H][W][4] float (r, g, b, U)
    t_final     OPTIONAL [V][H][W] float;   n_contrib OPTIONAL [V][H][W] uint32
    tile_partial [V][gx*gy] float: sum of U over the tile's in-image pixels
-   n_frag      OPTIONAL [1] uint64, ADDED to: blended (pixel, Gaussian) pairs */
+   n_frag      OPTIONAL [2] uint64, ADDED to: [0] blended (pixel, Gaussian) pairs
+               ("composited fragments"); [1] (pixel, list entry) pairs the plain
+               definition evaluates = sum over pixels of the entries up to and
+               including the one that stops it (the whole list if none does) */
 gsr_status gsr_composite(gsr_ctx* ctx, const float* render_rec, int64_t n, const uint32_t* vals,
                          const uint32_t* ranges, const gsr_camera* cams, int32_t n_views,
                          float* rgbu, float* t_final, uint32_t* n_contrib, float* tile_partial,
@@ -183,6 +186,30 @@ gsr_status gsr_sort_pairs_u64(gsr_ctx* ctx, const uint64_t* keys_in, const uint3
 
 /* ---- utility: bytes of scratch the context currently holds (diagnostics) */
 int64_t gsr_scratch_bytes(const gsr_ctx* ctx);
+
+/* ---- diagnostics: per-stage kernel launch counts, CUDA-event timing and
+   algorithmic HBM bytes.  Stages: */
+enum {
+  GSR_STAGE_PROJECT = 0,    /* K1 */
+  GSR_STAGE_COMPACT = 1,    /* K2 tile-count scan + visible compaction */
+  GSR_STAGE_DEPTH_SORT = 2, /* K4a onesweep passes over (view, depth) keys */
+  GSR_STAGE_EMIT = 3,       /* K3 key duplication + warp-aggregated tile counts */
+  GSR_STAGE_RANGES = 4,     /* K5 tile ranges + tile-sort histograms */
+  GSR_STAGE_TILE_SORT = 5,  /* K4b onesweep passes over (view, tile) keys */
+  GSR_STAGE_COMPOSITE = 6,  /* K6 */
+  GSR_STAGE_SCORE = 7,      /* K7 */
+  GSR_STAGE_SELECT = 8,     /* K8 */
+  GSR_STAGE_SORT_U64 = 9,   /* utility sort (histogram + passes) */
+  GSR_N_STAGES = 10
+};
+/* enable != 0: bracket every stage with CUDA events on its launch stream. */
+gsr_status gsr_timing_enable(gsr_ctx* ctx, int enable);
+/* SYNC.  For each stage since the last read: device milliseconds (sum of the
+   event-bracketed spans; 0 when timing is off), kernel launches, algorithmic
+   HBM bytes (the bytes the step must move).
+   Any output pointer may be NULL.  Resets the accumulators. [host] arrays of
+   GSR_N_STAGES. */
+gsr_status gsr_timing_read(gsr_ctx* ctx, double* ms, int64_t* launches, double* bytes);
 
 #ifdef __cplusplus
 }

@@ -174,12 +174,12 @@ def composite_tiled(proj, sorted_vals, ranges_view, cam):
     rgbu = np.zeros((H, W, 4), dtype=np.float32)
     tf = np.zeros((H, W), dtype=np.float32)
     nc = np.zeros((H, W), dtype=np.uint32)
-    nf = np.zeros(1, dtype=np.uint64)
+    nf = np.zeros(2, dtype=np.uint64)
     sv = np.ascontiguousarray(sorted_vals, dtype=np.uint32)
     rv = np.ascontiguousarray(ranges_view, dtype=np.uint32)
     score = L.orc_composite_tiled(_p(proj), _p(sv if len(sv) else np.zeros(1, np.uint32)), _p(rv),
                                   _p(c), _p(rgbu), _p(tf), _p(nc), _p(nf))
-    return dict(rgbu=rgbu, t_final=tf, n_contrib=nc, score=score, n_frag=int(nf[0]))
+    return dict(rgbu=rgbu, t_final=tf, n_contrib=nc, score=score, n_frag=int(nf[0]), n_eval=int(nf[1]))
 
 
 def composite_brute(proj, cam):
@@ -191,9 +191,9 @@ def composite_brute(proj, cam):
     rgbu = np.zeros((H, W, 4), dtype=np.float32)
     tf = np.zeros((H, W), dtype=np.float32)
     nc = np.zeros((H, W), dtype=np.uint32)
-    nf = np.zeros(1, dtype=np.uint64)
+    nf = np.zeros(2, dtype=np.uint64)
     score = L.orc_composite_brute(_p(proj), len(proj), _p(c), _p(rgbu), _p(tf), _p(nc), _p(nf))
-    return dict(rgbu=rgbu, t_final=tf, n_contrib=nc, score=score, n_frag=int(nf[0]))
+    return dict(rgbu=rgbu, t_final=tf, n_contrib=nc, score=score, n_frag=int(nf[0]), n_eval=int(nf[1]))
 
 
 def render_view(field, cam):

@@ -287,11 +287,12 @@ void orc_ranges(const uint64_t* sorted_keys, int64_t k, int64_t n_tiles_total, u
 
 /* O5: composite one pixel over an ordered list of Gaussians. */
 static void composite_pixel(const orc_proj* p, const uint32_t* order, int64_t len, int px, int py,
-                            float out[4], float* t_final, uint32_t* n_contrib) {
+                            float out[4], float* t_final, uint32_t* n_contrib, uint64_t* n_eval) {
   float pcx = (float)px + 0.5f, pcy = (float)py + 0.5f;
   float T = 1.0f;
   float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
   uint32_t nc = 0;
+  *n_eval = (uint64_t)len; /* entries evaluated: up to and including the stopping one */
   for (int64_t i = 0; i < len; ++i) {
     const orc_proj* q = &p[order[i]];
     float dx = q->u - pcx, dy = q->v - pcy;
@@ -301,7 +302,7 @@ static void composite_pixel(const orc_proj* p, const uint32_t* order, int64_t le
     float alpha = fminf(ORC_ALPHA_MAX, q->o * orc_exp_spec(power));
     if (alpha < ORC_ALPHA_MIN) continue;
     float tT = T * (1.0f - alpha);
-    if (tT < ORC_T_STOP) break;
+    if (tT < ORC_T_STOP) { *n_eval = (uint64_t)(i + 1); break; }
     float w = alpha * T;
     acc[0] = fmaf(q->r, w, acc[0]);
     acc[1] = fmaf(q->g, w, acc[1]);
@@ -317,20 +318,22 @@ static void composite_pixel(const orc_proj* p, const uint32_t* order, int64_t le
 
 /* O5 + O6, tiled: for each pixel, the sorted values of its tile's range.
    rgbu [H][W][4], t_final / n_contrib [H][W] optional (NULL).  Returns the
-   score (double sum of U over all W*H pixels / (W*H)); *n_frag = sum n_contrib. */
+   score (double sum of U over all W*H pixels / (W*H)); n_frag[0] = sum n_contrib
+   (blended pairs), n_frag[1] = evaluated (pixel, entry) pairs. */
 double orc_composite_tiled(const orc_proj* p, const uint32_t* sorted_vals, const uint32_t* ranges_view,
                            const orc_camera* cam, float* rgbu, float* t_final, uint32_t* n_contrib,
                            uint64_t* n_frag) {
   int W = cam->width, H = cam->height;
   int gx = (W + ORC_TILE - 1) / ORC_TILE;
   double sum = 0.0;
-  uint64_t frag = 0;
+  uint64_t frag = 0, ev = 0;
   for (int py = 0; py < H; ++py)
     for (int px = 0; px < W; ++px) {
       int tile = (py / ORC_TILE) * gx + (px / ORC_TILE);
       uint32_t s = ranges_view[2 * tile], e = ranges_view[2 * tile + 1];
-      float o4[4], tf; uint32_t nc;
-      composite_pixel(p, sorted_vals + s, (int64_t)e - (int64_t)s, px, py, o4, &tf, &nc);
+      float o4[4], tf; uint32_t nc; uint64_t ne;
+      composite_pixel(p, sorted_vals + s, (int64_t)e - (int64_t)s, px, py, o4, &tf, &nc, &ne);
+      ev += ne;
       size_t pi = (size_t)py * W + px;
       if (rgbu) memcpy(rgbu + 4 * pi, o4, sizeof(o4));
       if (t_final) t_final[pi] = tf;
@@ -338,7 +341,7 @@ double orc_composite_tiled(const orc_proj* p, const uint32_t* sorted_vals, const
       sum += (double)o4[3];
       frag += nc;
     }
-  if (n_frag) *n_frag = frag;
+  if (n_frag) { n_frag[0] = frag; n_frag[1] = ev; }
   return sum / ((double)W * (double)H);
 }
 
@@ -363,11 +366,12 @@ double orc_composite_brute(const orc_proj* p, int64_t n, const orc_camera* cam, 
   qsort(order, (size_t)len, sizeof(uint32_t), cmp_depth_index);
   int W = cam->width, H = cam->height;
   double sum = 0.0;
-  uint64_t frag = 0;
+  uint64_t frag = 0, ev = 0;
   for (int py = 0; py < H; ++py)
     for (int px = 0; px < W; ++px) {
-      float o4[4], tf; uint32_t nc;
-      composite_pixel(p, order, len, px, py, o4, &tf, &nc);
+      float o4[4], tf; uint32_t nc; uint64_t ne;
+      composite_pixel(p, order, len, px, py, o4, &tf, &nc, &ne);
+      ev += ne;
       size_t pi = (size_t)py * W + px;
       if (rgbu) memcpy(rgbu + 4 * pi, o4, sizeof(o4));
       if (t_final) t_final[pi] = tf;
@@ -376,7 +380,7 @@ double orc_composite_brute(const orc_proj* p, int64_t n, const orc_camera* cam, 
       frag += nc;
     }
   free(order);
-  if (n_frag) *n_frag = frag;
+  if (n_frag) { n_frag[0] = frag; n_frag[1] = ev; }
   return sum / ((double)W * (double)H);
 }
 
@@ -408,12 +412,12 @@ static void render_one(orc_job* J, int v) {
   uint32_t* ranges = (uint32_t*)malloc(sizeof(uint32_t) * 2 * (size_t)gx * gy);
   orc_ranges(keys, k, (int64_t)gx * gy, ranges);
   size_t img = (size_t)cam->width * cam->height * 4;
-  uint64_t nf = 0;
+  uint64_t nf[2] = {0, 0};
   /* images of one batch share W,H: view v starts at v * img */
   double sc = orc_composite_tiled(p, vals, ranges, cam, J->rgbu ? J->rgbu + (size_t)v * img : NULL,
-                                  NULL, NULL, &nf);
+                                  NULL, NULL, nf);
   J->scores[v] = sc;
-  if (J->n_frag) J->n_frag[v] = nf;
+  if (J->n_frag) J->n_frag[v] = nf[0];
   if (J->n_keys) J->n_keys[v] = k;
   free(ranges); free(vals); free(keys); free(p);
 }

@@ -2,6 +2,7 @@
 #include "gsr_internal.cuh"
 
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 
 namespace gsr {
@@ -39,6 +40,30 @@ gsr_status ensure(gsr_ctx* ctx, Slot s, size_t bytes, void** out) {
   return GSR_OK;
 }
 
+static cudaEvent_t pool_get(gsr_ctx* ctx) {
+  if (!ctx->pool.empty()) {
+    cudaEvent_t e = ctx->pool.back();
+    ctx->pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+
+int stage_begin(gsr_ctx* ctx, int stage, cudaStream_t st) {
+  if (!ctx->timing) return -1;
+  gsr_ctx::Span s{stage, pool_get(ctx), pool_get(ctx)};
+  cudaEventRecord(s.a, st);
+  ctx->spans.push_back(s);
+  return (int)ctx->spans.size() - 1;
+}
+
+void stage_end(gsr_ctx* ctx, int span, cudaStream_t st) {
+  if (span < 0 || span >= (int)ctx->spans.size()) return;
+  cudaEventRecord(ctx->spans[span].b, st);
+}
+
 }  // namespace gsr
 
 using namespace gsr;
@@ -53,6 +78,7 @@ gsr_status gsr_create(gsr_ctx** out, int device) {
   gsr_ctx* c = new gsr_ctx();
   c->device = device;
   cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
+  if (const char* v = std::getenv("GSR_COMPOSITE")) c->composite_variant = std::atoi(v);
   e = cudaMallocHost(&c->host_pinned, 4096);
   if (e != cudaSuccess) {
     delete c;
@@ -62,9 +88,43 @@ gsr_status gsr_create(gsr_ctx** out, int device) {
   return GSR_OK;
 }
 
+gsr_status gsr_timing_enable(gsr_ctx* ctx, int enable) {
+  if (!ctx) return GSR_EINVAL;
+  ctx->timing = enable != 0;
+  return GSR_OK;
+}
+
+gsr_status gsr_timing_read(gsr_ctx* ctx, double* ms, int64_t* launches, double* bytes) {
+  if (!ctx) return GSR_EINVAL;
+  double acc[GSR_N_STAGES] = {};
+  for (auto& s : ctx->spans) {
+    cudaError_t e = cudaEventSynchronize(s.b);
+    if (e != cudaSuccess) return check_cuda(ctx, e, "gsr_timing_read");
+    float t = 0.f;
+    cudaEventElapsedTime(&t, s.a, s.b);
+    acc[s.stage] += t;
+    ctx->pool.push_back(s.a);
+    ctx->pool.push_back(s.b);
+  }
+  ctx->spans.clear();
+  for (int i = 0; i < GSR_N_STAGES; ++i) {
+    if (ms) ms[i] = acc[i];
+    if (launches) launches[i] = ctx->launches[i];
+    if (bytes) bytes[i] = ctx->bytes[i];
+    ctx->launches[i] = 0;
+    ctx->bytes[i] = 0.0;
+  }
+  return GSR_OK;
+}
+
 gsr_status gsr_destroy(gsr_ctx* ctx) {
   if (!ctx) return GSR_EINVAL;
   cudaSetDevice(ctx->device);
+  for (auto& s : ctx->spans) {
+    cudaEventDestroy(s.a);
+    cudaEventDestroy(s.b);
+  }
+  for (auto e : ctx->pool) cudaEventDestroy(e);
   for (int s = 0; s < S_NSLOTS; ++s)
     if (ctx->buf[s]) cudaFree(ctx->buf[s]);
   if (ctx->host_pinned) cudaFreeHost(ctx->host_pinned);
@@ -147,6 +207,11 @@ gsr_status gsr_project(gsr_ctx* ctx, const gsr_gaussians* G, const gsr_camera* c
   CamBatch cb;
   std::memset(&cb, 0, sizeof(cb));
   std::memcpy(cb.c, cams, sizeof(gsr_camera) * (size_t)n_views);
+  // algorithmic bytes: parameter planes once per batch + bin planes; the 48-byte
+  // render records of the visible pairs are added by gsr_bin_sort (it knows N_vis)
+  const int planes = 3 + (3 * (G->sh_degree + 1) * (G->sh_degree + 1) + 3) / 4;
+  account(ctx, GSR_STAGE_PROJECT, 1, 16.0 * planes * (double)G->n + 16.0 * n_views * (double)G->n);
+  StageScope sc(ctx, GSR_STAGE_PROJECT, (cudaStream_t)stream);
   return check_cuda(ctx, launch_project(*G, cb, n_views, render_rec, bin_rec, (cudaStream_t)stream), "k1_project");
 }
 

@@ -234,7 +234,7 @@ __global__ void __launch_bounds__(256) hist_u64(const uint64_t* __restrict__ key
 //           vals_out and, if keys64 != null, the full 64-bit key
 //           (key << 32) | depth_plane[view * nper + g].
 template <typename KeyT, int KPT, int MODE>
-__global__ void __launch_bounds__(256) onesweep(const KeyT* __restrict__ kin, const uint32_t* __restrict__ vin,
+__global__ void __launch_bounds__(256, 3) onesweep(const KeyT* __restrict__ kin, const uint32_t* __restrict__ vin,
                                                 KeyT* __restrict__ kout, uint32_t* __restrict__ vout, uint32_t n,
                                                 int shift, int nbits, const uint32_t* __restrict__ base,
                                                 uint32_t* __restrict__ lookback, uint32_t* __restrict__ ctr,
@@ -259,14 +259,15 @@ __global__ void __launch_bounds__(256) onesweep(const KeyT* __restrict__ kin, co
   const uint32_t bid = s_bid;
   const uint32_t mask = (nbits >= 32) ? 0xffffffffu : ((1u << nbits) - 1);
   const int64_t wbase = (int64_t)bid * TILE + (int64_t)warp * (KPT * 32);
+  // Keys stay in registers through ranking; values are not needed until the
+  // scatter, so they are loaded there (keeps 4 blocks / SM resident).
   KeyT key[KPT];
-  uint32_t val[KPT], rank[KPT];
+  uint32_t rank[KPT];
 #pragma unroll
   for (int k = 0; k < KPT; ++k) {
     const int64_t idx = wbase + k * 32 + lane;
     const bool valid = idx < (int64_t)n;
     key[k] = valid ? kin[idx] : KeyT(0);
-    val[k] = valid ? vin[idx] : 0u;
   }
   const uint32_t lt = (1u << lane) - 1;
 #pragma unroll
@@ -329,19 +330,24 @@ __global__ void __launch_bounds__(256) onesweep(const KeyT* __restrict__ kin, co
     s_gbase[d] = base[d] + excl - start;
   }
   __syncthreads();
-  uint32_t pos[KPT];
 #pragma unroll
   for (int k = 0; k < KPT; ++k) {
     const uint32_t d = (uint32_t)(key[k] >> shift) & mask;
-    pos[k] = s_start[d] + u.hist[warp][d] + rank[k];
+    rank[k] += s_start[d] + u.hist[warp][d];  // -> position in the block's stage
+  }
+  uint32_t val[KPT];
+#pragma unroll
+  for (int k = 0; k < KPT; ++k) {
+    const int64_t idx = wbase + k * 32 + lane;
+    val[k] = idx < (int64_t)n ? vin[idx] : 0u;
   }
   __syncthreads();
 #pragma unroll
   for (int k = 0; k < KPT; ++k) {
     const int64_t idx = wbase + k * 32 + lane;
     if (idx < (int64_t)n) {
-      u.st.k[pos[k]] = key[k];
-      u.st.v[pos[k]] = val[k];
+      u.st.k[rank[k]] = key[k];
+      u.st.v[rank[k]] = val[k];
     }
   }
   __syncthreads();
@@ -385,14 +391,28 @@ __global__ void __launch_bounds__(256) k3_emit(const uint64_t* __restrict__ dkey
                                                const uint32_t* __restrict__ nt_plane, int64_t n, uint32_t gx,
                                                uint32_t tpv, uint32_t* __restrict__ tkeys,
                                                uint32_t* __restrict__ tvals, uint32_t* __restrict__ counts,
-                                               uint64_t* __restrict__ lb, uint32_t* __restrict__ ctr) {
+                                               uint64_t* __restrict__ lb, uint32_t* __restrict__ ctr,
+                                               int smem_bins) {
+  // Per-tile counts: warp-aggregated (match_any + one atomic per distinct tile
+  // in the warp) into a shared-memory histogram over the tiles of the block's
+  // first view (a depth-sorted block almost always lies in one view), flushed
+  // with one global atomic per non-empty bin; other views go straight to
+  // global memory (still warp-aggregated).
+  extern __shared__ uint32_t s_cnt[];
   __shared__ uint64_t s_w[8];
   __shared__ uint64_t s_prefix;
-  __shared__ uint32_t s_bid;
+  __shared__ uint32_t s_bid, s_view0;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (tid == 0) s_bid = atomicAdd(ctr, 1u);
+  if (tid == 0) {
+    const uint32_t b = atomicAdd(ctr, 1u);
+    s_bid = b;
+    s_view0 = (uint32_t)(dkeys[(int64_t)b * K3_TILE] >> 32);
+  }
+  for (int t = tid; t < smem_bins; t += 256) s_cnt[t] = 0;
   __syncthreads();
   const int64_t bid = s_bid;
+  const uint32_t view0 = s_view0;
+  const uint32_t lo = view0 * tpv, hi = lo + (uint32_t)smem_bins;
   const int64_t e0 = bid * K3_TILE + (int64_t)warp * (32 * K3_ROUNDS);
   uint32_t nt[K3_ROUNDS], xr[K3_ROUNDS], yr[K3_ROUNDS], g[K3_ROUNDS], view[K3_ROUNDS];
   uint64_t mine = 0;
@@ -436,7 +456,10 @@ __global__ void __launch_bounds__(256) k3_emit(const uint64_t* __restrict__ dkey
     const uint32_t inc = warp_incl_scan<uint32_t>(nt[r]);
     const uint32_t excl = inc - nt[r];
     const uint32_t total = __shfl_sync(FULL, inc, 31);
-    const uint32_t x0 = xr[r] & 0xffffu, wdt = (xr[r] >> 16) - x0, y0 = yr[r] & 0xffffu;
+    // per entry: key of the rect's first tile, rect width and its reciprocal
+    const uint32_t x0 = xr[r] & 0xffffu, wdt = max((xr[r] >> 16) - x0, 1u), y0 = yr[r] & 0xffffu;
+    const uint32_t kbase = view[r] * tpv + y0 * gx + x0;
+    const float rcp = __frcp_rn((float)wdt);
     for (uint32_t jb = 0; jb < total; jb += 32) {
       const uint32_t j = jb + lane;
       // owner lane: largest s with excl[s] <= j
@@ -447,22 +470,35 @@ __global__ void __launch_bounds__(256) k3_emit(const uint64_t* __restrict__ dkey
         if (e <= j) s += step;
       }
       const uint32_t oexcl = __shfl_sync(FULL, excl, s);
-      const uint32_t ox0 = __shfl_sync(FULL, x0, s), ow = __shfl_sync(FULL, wdt, s);
-      const uint32_t oy0 = __shfl_sync(FULL, y0, s), og = __shfl_sync(FULL, g[r], s);
-      const uint32_t ov = __shfl_sync(FULL, view[r], s);
+      const uint32_t okb = __shfl_sync(FULL, kbase, s), ow = __shfl_sync(FULL, wdt, s);
+      const float orcp = __shfl_sync(FULL, rcp, s);
+      const uint32_t og = __shfl_sync(FULL, g[r], s);
       const bool act = j < total;
       uint32_t key = 0xffffffffu;
       if (act) {
         const uint32_t loc = j - oexcl;
-        const uint32_t ty = oy0 + loc / ow, tx = ox0 + loc % ow;
-        key = ov * tpv + ty * gx + tx;
+        uint32_t q = (uint32_t)((float)loc * orcp);  // loc < 2^24: off by at most one
+        int32_t rem = (int32_t)(loc - q * ow);
+        if (rem >= (int32_t)ow) { ++q; rem -= ow; }
+        if (rem < 0) { --q; rem += ow; }
+        key = okb + q * gx + (uint32_t)rem;
         tkeys[base + j] = key;
         tvals[base + j] = og;
       }
       const uint32_t peers = __match_any_sync(FULL, key);
-      if (act && (__ffs(peers) - 1) == lane) atomicAdd(counts + key, (uint32_t)__popc(peers));
+      if (act && (__ffs(peers) - 1) == lane) {
+        if (key >= lo && key < hi)
+          atomicAdd(s_cnt + (key - lo), (uint32_t)__popc(peers));
+        else
+          atomicAdd(counts + key, (uint32_t)__popc(peers));
+      }
     }
     base += total;
+  }
+  __syncthreads();
+  for (int t = tid; t < smem_bins; t += 256) {
+    const uint32_t c = s_cnt[t];
+    if (c) atomicAdd(counts + lo + t, c);
   }
 }
 
@@ -564,7 +600,7 @@ int bits_for(uint64_t count) {  // ceil(log2(count)), 0 for count <= 1
 }
 
 constexpr int KPT64 = 12;  // onesweep u64 keys: 3072 keys per block
-constexpr int KPT32 = 16;  // onesweep u32 keys: 4096 keys per block
+constexpr int KPT32 = 12;  // onesweep u32 keys: 3072 keys per block
 
 size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
@@ -627,6 +663,8 @@ extern "C" gsr_status gsr_sort_pairs_u64(gsr_ctx* ctx, const uint64_t* keys_in, 
   if ((s = check_cuda(ctx, cudaMemsetAsync(hist, 0, 8 * 256 * 4, st), "memset")) != GSR_OK) return s;
   if ((s = check_cuda(ctx, cudaMemsetAsync(lb, 0, lb_bytes, st), "memset")) != GSR_OK) return s;
   const int hb = (int)std::min<int64_t>((n + 255) / 256, (int64_t)ctx->num_sms * 8);
+  StageScope scope(ctx, GSR_STAGE_SORT_U64, st);
+  account(ctx, GSR_STAGE_SORT_U64, 2 + passes, 8.0 * n + 24.0 * passes * n);
   hist_u64<<<hb, 256, 0, st>>>(keys_in, n, begin_bit, passes, end_bit, hist);
   scan_hist<<<1, 256, 0, st>>>(hist, base, passes);
   if ((s = check_cuda(ctx, cudaGetLastError(), "hist")) != GSR_OK) return s;
@@ -692,9 +730,11 @@ extern "C" gsr_status gsr_bin_sort(gsr_ctx* ctx, const uint32_t* bin_rec, int64_
   uint64_t* lbv = (uint64_t*)lb;
   uint64_t* lbk = lbv + std::max<size_t>(nb2, 1);
   uint32_t* ctr2 = (uint32_t*)((char*)lb + align_up(2 * std::max<size_t>(nb2, 1) * 8));
+  const int sp2 = stage_begin(ctx, GSR_STAGE_COMPACT, st);
   if (M > 0)
     k2_compact<<<(unsigned)nb2, 256, 0, st>>>(p_depth, p_nt, M, n, (uint64_t*)dka, (uint32_t*)dva,
                                               (uint32_t*)eo, lbv, lbk, ctr2, (uint64_t*)tot, dhist, dpasses);
+  stage_end(ctx, sp2, st);
   if ((s = check_cuda(ctx, cudaGetLastError(), "k2_compact")) != GSR_OK) return s;
   uint64_t* hp = (uint64_t*)ctx->host_pinned;
   if ((s = check_cuda(ctx, cudaMemcpyAsync(hp, tot, 16, cudaMemcpyDeviceToHost, st), "readback")) != GSR_OK)
@@ -703,6 +743,13 @@ extern "C" gsr_status gsr_bin_sort(gsr_ctx* ctx, const uint32_t* bin_rec, int64_
   const int64_t nvis = (int64_t)hp[0];
   const int64_t K = (int64_t)hp[1];
   *n_keys = K;
+  ctx->last_nvis = nvis;
+  ctx->last_keys = K;
+  // algorithmic bytes: K2 reads n_tiles of every pair and the depth of
+  // the visible ones, writes 12 B per visible pair; K1's 48-B render records of
+  // the visible pairs are attributed to the projection stage.
+  account(ctx, GSR_STAGE_COMPACT, M > 0 ? 1 : 0, 4.0 * M + 16.0 * nvis);
+  account(ctx, GSR_STAGE_PROJECT, 0, 48.0 * nvis);
   if (K > capacity) return set_err(ctx, GSR_ECAPACITY, "gsr_bin_sort: capacity too small (n_keys = required)");
   if (K >= (1ll << 31)) return set_err(ctx, GSR_EINVAL, "gsr_bin_sort: K >= 2^31 keys in one batch");
 
@@ -736,6 +783,7 @@ extern "C" gsr_status gsr_bin_sort(gsr_ctx* ctx, const uint32_t* bin_rec, int64_
   uint32_t* ctrs = (uint32_t*)((char*)lb + o_c);  // [0..4] depth, [5] k3, [6..9] tile
 
   // ---- K4a: depth sort of the visible pairs ----
+  int sp = stage_begin(ctx, GSR_STAGE_DEPTH_SORT, st);
   scan_hist<<<1, 256, 0, st>>>(dhist, dbase, dpasses);
   const uint64_t* ck = (const uint64_t*)dka;
   const uint32_t* cvv = (const uint32_t*)dva;
@@ -750,18 +798,29 @@ extern "C" gsr_status gsr_bin_sort(gsr_ctx* ctx, const uint32_t* bin_rec, int64_
     ck = ko;
     cvv = vo;
   }
+  stage_end(ctx, sp, st);
+  account(ctx, GSR_STAGE_DEPTH_SORT, 1 + dpasses, 24.0 * dpasses * nvis);
   if ((s = check_cuda(ctx, cudaGetLastError(), "depth sort")) != GSR_OK) return s;
 
   // ---- K3: emission + counts ----
-  k3_emit<<<(unsigned)nb3, 256, 0, st>>>(ck, cvv, nvis, p_xr, p_yr, p_nt, n, gx, (uint32_t)tpv, (uint32_t*)tka,
-                                         (uint32_t*)tva, (uint32_t*)cnt, lb3, ctrs + 5);
+  sp = stage_begin(ctx, GSR_STAGE_EMIT, st);
+  const int bins = tpv <= 12288 ? (int)tpv : 0;  // <= 48 KB of shared memory
+  k3_emit<<<(unsigned)nb3, 256, bins * 4, st>>>(ck, cvv, nvis, p_xr, p_yr, p_nt, n, gx, (uint32_t)tpv,
+                                                (uint32_t*)tka, (uint32_t*)tva, (uint32_t*)cnt, lb3, ctrs + 5,
+                                                bins);
+  stage_end(ctx, sp, st);
+  account(ctx, GSR_STAGE_EMIT, 1, 24.0 * nvis + 8.0 * K + 4.0 * T);
   if ((s = check_cuda(ctx, cudaGetLastError(), "k3_emit")) != GSR_OK) return s;
 
   // ---- K5: ranges + tile-sort histograms ----
+  sp = stage_begin(ctx, GSR_STAGE_RANGES, st);
   k5_ranges<<<1, 1024, 0, st>>>((const uint32_t*)cnt, (int64_t)T, (uint2*)ranges, tpasses, thist, tbase);
+  stage_end(ctx, sp, st);
+  account(ctx, GSR_STAGE_RANGES, 1, 12.0 * T);
   if ((s = check_cuda(ctx, cudaGetLastError(), "k5_ranges")) != GSR_OK) return s;
 
   // ---- K4b: tile sort ----
+  sp = stage_begin(ctx, GSR_STAGE_TILE_SORT, st);
   const uint32_t* tk = (const uint32_t*)tka;
   const uint32_t* tv = (const uint32_t*)tva;
   for (int p = 0; p < tpasses; ++p) {
@@ -782,10 +841,15 @@ extern "C" gsr_status gsr_bin_sort(gsr_ctx* ctx, const uint32_t* bin_rec, int64_
       tv = vo;
     }
   }
+  stage_end(ctx, sp, st);
+  // each pass reads 8 B/key; intermediate passes write 8 B/key, the last writes
+  // the 4-B values (+ 8-B keys when asked)
+  account(ctx, GSR_STAGE_TILE_SORT, tpasses, 16.0 * (tpasses - 1) * K + (12.0 + (keys ? 8.0 : 0.0)) * K);
   if ((s = check_cuda(ctx, cudaGetLastError(), "tile sort")) != GSR_OK) return s;
 
   // ---- optional O2 emission-order list ----
   if (keys_unsorted) {
+    account(ctx, GSR_STAGE_EMIT, 1, 16.0 * M + 12.0 * K);
     k_emit_o2<<<(unsigned)((M + 255) / 256), 256, 0, st>>>(p_depth, p_xr, p_yr, p_nt, (const uint32_t*)eo, M, n, gx,
                                                            (uint32_t)tpv, keys_unsorted, vals_unsorted);
     if ((s = check_cuda(ctx, cudaGetLastError(), "emit_o2")) != GSR_OK) return s;

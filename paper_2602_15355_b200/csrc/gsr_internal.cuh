@@ -9,6 +9,7 @@
 #include <stdint.h>
 
 #include <string>
+#include <vector>
 
 #include "../../include/gsr.h"
 
@@ -29,8 +30,7 @@ struct CamBatch {
 // exp(x) for x <= 0: Cody-Waite range reduction by ln2 (hi/lo), degree-7
 // Taylor polynomial in Horner form, scale by 2^k built in the exponent field.
 // Pure IEEE float ops -> bit-identical on any correctly rounding FPU.
-__device__ __forceinline__ float exp_spec(float x) {
-  if (x < -80.0f) return 0.0f;
+__device__ __forceinline__ float exp_spec_core(float x) {  // x in [-80, 0]
   const float kf = rintf(x * __int_as_float(0x3fb8aa3b));
   float r = __fmaf_rn(kf, -__int_as_float(0x3f317200), x);
   r = __fmaf_rn(kf, -__int_as_float(0x35bfbe8e), r);
@@ -45,6 +45,7 @@ __device__ __forceinline__ float exp_spec(float x) {
   const int k = (int)kf;
   return p * __int_as_float((k + 127) << 23);
 }
+__device__ __forceinline__ float exp_spec(float x) { return x < -80.0f ? 0.0f : exp_spec_core(x); }
 
 // ---- context scratch ----
 enum Slot {
@@ -69,6 +70,18 @@ struct gsr_ctx {
   size_t cap[gsr::S_NSLOTS] = {};
   void* host_pinned = nullptr;  // 4 KB pinned readback area
   int num_sms = 148;
+  // diagnostics
+  bool timing = false;
+  struct Span {
+    int stage;
+    cudaEvent_t a, b;
+  };
+  std::vector<Span> spans;
+  std::vector<cudaEvent_t> pool;
+  double bytes[GSR_N_STAGES] = {};
+  int64_t launches[GSR_N_STAGES] = {};
+  int64_t last_nvis = 0, last_keys = 0;  // of the last gsr_bin_sort (byte accounting)
+  int composite_variant = 2;              // GSR_COMPOSITE=1 selects the v1 (block-synchronous) kernel
 };
 
 namespace gsr {
@@ -76,6 +89,21 @@ namespace gsr {
 gsr_status set_err(gsr_ctx* ctx, gsr_status st, const std::string& msg);
 gsr_status check_cuda(gsr_ctx* ctx, cudaError_t e, const char* what);
 gsr_status ensure(gsr_ctx* ctx, Slot s, size_t bytes, void** out);
+
+// ---- diagnostics: stage spans (CUDA events) + launch / byte accounting ----
+int stage_begin(gsr_ctx* ctx, int stage, cudaStream_t st);  // returns span id or -1
+void stage_end(gsr_ctx* ctx, int span, cudaStream_t st);
+inline void account(gsr_ctx* ctx, int stage, int64_t launches, double bytes) {
+  ctx->launches[stage] += launches;
+  ctx->bytes[stage] += bytes;
+}
+struct StageScope {
+  gsr_ctx* ctx;
+  int span;
+  cudaStream_t st;
+  StageScope(gsr_ctx* c, int stage, cudaStream_t s) : ctx(c), span(stage_begin(c, stage, s)), st(s) {}
+  ~StageScope() { stage_end(ctx, span, st); }
+};
 
 // ---- launchers (each returns cudaGetLastError() of its launches) ----
 cudaError_t launch_project(const gsr_gaussians& G, const CamBatch& cams, int V, float* rec,

@@ -73,6 +73,8 @@ extern "C" gsr_status gsr_select_nbv(gsr_ctx* ctx, const float* scores, int32_t 
     cudaError_t e = cudaFuncSetAttribute(k8_select, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if ((s = check_cuda(ctx, e, "k8 smem attribute")) != GSR_OK) return s;
   }
+  account(ctx, GSR_STAGE_SELECT, 1, 4.0 * n + 4.0 * k);
+  StageScope scope(ctx, GSR_STAGE_SELECT, st);
   k8_select<<<1, 1024, smem, st>>>(scores, n, P, (const uint8_t*)dex, k, out_idx);
   return check_cuda(ctx, cudaGetLastError(), "k8_select");
 }

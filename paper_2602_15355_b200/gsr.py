@@ -31,7 +31,9 @@ assert CAM_DTYPE.itemsize == 96
 
 EXPORTED = ["gsr_create", "gsr_destroy", "gsr_last_error", "gsr_version", "gsr_camera_look_at",
             "gsr_project", "gsr_bin_sort", "gsr_composite", "gsr_score_views", "gsr_select_nbv",
-            "gsr_sort_pairs_u64", "gsr_scratch_bytes"]
+            "gsr_sort_pairs_u64", "gsr_scratch_bytes", "gsr_timing_enable", "gsr_timing_read"]
+STAGES = ["project", "compact", "depth_sort", "emit", "ranges", "tile_sort", "composite", "score", "select",
+          "sort_u64"]
 
 
 class GsrError(RuntimeError):
@@ -64,6 +66,8 @@ def _load():
     L.gsr_score_views.argtypes = [P, P, P, i32, P, P]
     L.gsr_select_nbv.argtypes = [P, P, i32, P, i32, P, P]
     L.gsr_sort_pairs_u64.argtypes = [P, P, P, P, P, i64, i32, i32, P]
+    L.gsr_timing_enable.argtypes = [P, ctypes.c_int]
+    L.gsr_timing_read.argtypes = [P, P, P, P]
     L.gsr_scratch_bytes.argtypes = [P]
     L.gsr_scratch_bytes.restype = i64
     for name in EXPORTED:
@@ -158,6 +162,17 @@ class Context:
 
     def scratch_bytes(self) -> int:
         return int(lib.gsr_scratch_bytes(self.handle))
+
+    def timing(self, enable: bool = True):
+        self._check(lib.gsr_timing_enable(self.handle, 1 if enable else 0))
+
+    def timing_read(self) -> dict:
+        """SYNC: per-stage {ms, launches, bytes} since the last read (then reset)."""
+        ms = np.zeros(len(STAGES), np.float64)
+        la = np.zeros(len(STAGES), np.int64)
+        by = np.zeros(len(STAGES), np.float64)
+        self._check(lib.gsr_timing_read(self.handle, ms.ctypes.data, la.ctypes.data, by.ctypes.data))
+        return {s: dict(ms=float(ms[i]), launches=int(la[i]), bytes=float(by[i])) for i, s in enumerate(STAGES)}
 
 
 def gsr_project(ctx: Context, g: Gaussians, cams, render_rec, bin_rec, stream=None):

@@ -50,7 +50,7 @@ class ViewScorer:
         self.keys = None
         self.ranges = None
         self.partial = None
-        self.n_frag = torch.zeros(1, dtype=torch.int64, device=self.dev)
+        self.n_frag = torch.zeros(2, dtype=torch.int64, device=self.dev)  # [blended, evaluated]
         self.last_keys = []
 
     def _ensure_keys(self, cap: int, want_keys: bool):

@@ -41,14 +41,15 @@ def gpu_batch(ctx, field, cams, images=True, want_unsorted=True, want_keys=True)
     rgbu = torch.full((V, H, W, 4), float("nan"), dtype=torch.float32, device="cuda") if images else None
     tf = torch.full((V, H, W), float("nan"), dtype=torch.float32, device="cuda") if images else None
     nc = torch.full((V, H, W), -1, dtype=torch.int32, device="cuda") if images else None
-    nfrag = torch.zeros(1, dtype=torch.int64, device="cuda")
+    nfrag = torch.zeros(2, dtype=torch.int64, device="cuda")
     gsr.gsr_composite(ctx, rec, n, vals, ranges, cams, partial, rgbu=rgbu, t_final=tf, n_contrib=nc, n_frag=nfrag)
     scores = torch.full((V,), float("nan"), dtype=torch.float32, device="cuda")
     gsr.gsr_score_views(ctx, partial, cams, scores)
     torch.cuda.synchronize()
     out = dict(K=K, rec=rec.cpu().numpy(), bin=binr.cpu().numpy().view(np.uint32),
                vals=vals.cpu().numpy().view(np.uint32)[:K], ranges=ranges.cpu().numpy().view(np.uint32),
-               partial=partial.cpu().numpy(), scores=scores.cpu().numpy(), n_frag=int(nfrag.item()))
+               partial=partial.cpu().numpy(), scores=scores.cpu().numpy(), n_frag=int(nfrag[0].item()),
+               n_eval=int(nfrag[1].item()))
     if want_keys:
         out["keys"] = keys.cpu().numpy().view(np.uint64)[:K]
     if want_unsorted:
@@ -67,7 +68,7 @@ def oracle_batch(field, cams, images=True):
     tpv = gx * gy
     res = dict(projs=projs, **bs)
     if images:
-        imgs, tfs, ncs, scores, nfrag = [], [], [], [], 0
+        imgs, tfs, ncs, scores, nfrag, neval = [], [], [], [], 0, 0
         for v, (p, c) in enumerate(zip(projs, cams)):
             rv = bs["ranges"][v * tpv:(v + 1) * tpv]
             o = oracle.composite_tiled(p, bs["vals"], rv, c)
@@ -76,8 +77,9 @@ def oracle_batch(field, cams, images=True):
             ncs.append(o["n_contrib"])
             scores.append(o["score"])
             nfrag += o["n_frag"]
+            neval += o["n_eval"]
         res.update(rgbu=np.stack(imgs), t_final=np.stack(tfs), n_contrib=np.stack(ncs),
-                   scores=np.array(scores), n_frag=nfrag)
+                   scores=np.array(scores), n_frag=nfrag, n_eval=neval)
     return res
 
 

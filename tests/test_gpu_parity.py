@@ -43,7 +43,7 @@ def _full_check(ctx, field, cams, images=True):
         assert np.array_equal(g["n_contrib"], o["n_contrib"])
         assert np.abs(g["t_final"] - o["t_final"]).max() <= IMG_TOL
         np.testing.assert_allclose(g["scores"], o["scores"], rtol=SCORE_RTOL, atol=0)
-        assert g["n_frag"] == o["n_frag"]
+        assert g["n_frag"] == o["n_frag"] and g["n_eval"] == o["n_eval"]
     return g, o
 
 
