@@ -79,6 +79,7 @@ gsr_status gsr_create(gsr_ctx** out, int device) {
   c->device = device;
   cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
   if (const char* v = std::getenv("GSR_COMPOSITE")) c->composite_variant = std::atoi(v);
+  if (const char* v = std::getenv("GSR_SORT")) c->sort_variant = std::atoi(v);
   e = cudaMallocHost(&c->host_pinned, 4096);
   if (e != cudaSuccess) {
     delete c;

@@ -81,7 +81,8 @@ struct gsr_ctx {
   double bytes[GSR_N_STAGES] = {};
   int64_t launches[GSR_N_STAGES] = {};
   int64_t last_nvis = 0, last_keys = 0;  // of the last gsr_bin_sort (byte accounting)
-  int composite_variant = 2;              // GSR_COMPOSITE=1 selects the v1 (block-synchronous) kernel
+  int sort_variant = 2;       // sort pass: 1 onesweep, 2 persistent onesweep (default), 3 reduce-then-scan (GSR_SORT)
+  int composite_variant = 3;  // K6 loader: 1 block-sync LDG, 2 TMA bulk/record, 3 TMA gather4, 4 cp.async
 };
 
 namespace gsr {
