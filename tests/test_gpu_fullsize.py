@@ -1,0 +1,75 @@
+"""Parity at BASELINE.json's full sizes, in the launch configuration bench.py
+times (ViewScorer, 16-view batches), on sampled views the oracle can render
+(one view per host thread).  Bar: images <= 1e-4 abs per channel, scores
+<= 1e-4 relative, same NBV over the sample unless the top-2 tie within 1e-4."""
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+THREADS = os.cpu_count() or 1
+
+
+def _gpu_images(field, cams, batch_views=16):
+    from paper_2602_15355_b200 import Gaussians
+    from paper_2602_15355_b200.pipeline import ViewScorer
+    G = Gaussians(torch.from_numpy(field.planes).cuda(), field.sh_degree)
+    sc = ViewScorer(G, batch_views=batch_views)
+    W, H = int(cams[0]["width"]), int(cams[0]["height"])
+    out_img, out_sc = [], []
+    for b0 in range(0, len(cams), batch_views):
+        c = cams[b0:b0 + batch_views]
+        img = torch.empty((len(c), H, W, 4), device="cuda")
+        s = torch.empty(len(c), device="cuda")
+        sc.run_batch(c, s, images=img)
+        out_img.append(img.cpu().numpy())
+        out_sc.append(s.cpu().numpy())
+    torch.cuda.synchronize()
+    return np.concatenate(out_img), np.concatenate(out_sc), sc
+
+
+def _check(field, cams, tag):
+    img, sc, scorer = _gpu_images(field, cams)
+    ref, _, _, rimg = oracle.render_views(field, cams, n_threads=THREADS, images=True)
+    d = np.abs(img.astype(np.float64) - rimg)
+    assert d.max() <= 1e-4, (tag, d.max())
+    np.testing.assert_allclose(sc, ref, rtol=1e-4, atol=0)
+    top = np.argsort(-ref, kind="stable")
+    if len(ref) > 1 and ref[top[0]] - ref[top[1]] > 1e-4 * abs(ref[top[0]]):
+        assert int(np.argmax(sc)) == int(top[0])
+    return img, sc, scorer
+
+
+def test_config3_sampled_views_full_size():
+    """configs[2]: 1M Gaussians, 800x800, f = 900; 16 strided views of the 1,024,
+    one 16-view batch (the bench's batch size); then the scores of the same
+    views inside a full 1,024-view scoring pass are bit-identical."""
+    scene = synth.make_scene(3)
+    idx = np.linspace(0, 1023, 16).round().astype(np.int64)
+    img, sc, scorer = _check(scene.field, scene.cameras[idx], "c3")
+    full = scorer.score_views(scene.cameras).cpu().numpy()
+    assert np.array_equal(full[idx], sc)
+    assert np.all(np.isfinite(full)) and np.all(full >= 0)
+
+
+def test_config4_wang_tiles_sampled_views():
+    """configs[3]: 8 x 500k-Gaussian tiles in a 4x4 Wang assembly (8M), 1920x1080."""
+    scene = synth.make_scene(4)
+    _check(scene.field, scene.cameras[[0, 21, 42, 63]], "c4")
+
+
+def test_config5_hierarchical_sampled_views():
+    """configs[4]: 2M Gaussians; coarse 256x256 (f = 288) and fine 1024x1024
+    (f = 1152) passes on sampled views."""
+    scene = synth.make_scene(5)
+    coarse = scene.cameras[np.linspace(0, 4095, 32).round().astype(np.int64)]
+    _, csc, _ = _check(scene.field, coarse, "c5-coarse")
+    top = np.argsort(-csc, kind="stable")[:4]
+    fine = synth.with_resolution(coarse[top], 1024, 1024, 1152.0)
+    _check(scene.field, fine, "c5-fine")
