@@ -57,6 +57,13 @@ def load_peaks():
     return dict(hbm_gbs=6650.0, sm_max_mhz=1965.0, source="fallback")
 
 
+def load_traffic():
+    """DRAM bytes (read + write) per launch of the roofline kernels, from the
+    committed ncu --set full capture (profiles/traffic.json), or {}."""
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    return json.load(open(path)) if os.path.exists(path) else {}
+
+
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
     Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
@@ -242,7 +249,6 @@ def main():
     clocks.start()
     ms, wall_ms, frags, stages = timed(args.steps, stage_timing=True)
     clk = clocks.stop()
-    ms_t, _, _, _ = (ms, None, None, None)
     # value: whole-job views/s, device time max over ranks
     views_per_s = 1024 * args.steps / (ms / 1e3)
     frag_per_s = frags[0] / (ms / 1e3)
@@ -265,29 +271,41 @@ def main():
                      "GB_per_s": round(st_by[k] / (st_ms[k] / 1e3) / 1e9, 1) if st_ms[k] > 0 else None,
                      "launches_per_step": stages[k]["launches"] / args.steps}
                  for k in stages if stages[k]["launches"]}
-    # roofline of the dominant HBM-bound kernel stage (largest device time among
-    # the sort / bin / projection stages) and of the composite (ALU) stage
-    hbm_stages = ["project", "compact", "depth_sort", "emit", "ranges", "tile_sort"]
-    dom = max(hbm_stages, key=lambda s: st_ms[s])
-    top = max(st_ms, key=lambda s: st_ms[s])
-    ach = st_by[dom] / (st_ms[dom] / 1e3) / 1e9
-    roof = {"bound": "hbm", "kernel": dom, "achieved": round(ach, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
-            "frac": round(ach / peaks["hbm_gbs"], 4), "traffic": None,
-            "peak_source": peaks["source"] + " hbm_gbs (MEASURED_PEAKS.json)",
-            "dominant_stage_of_step": top}
-    if top == "composite":
-        # K6 is bound by the issue rate of FP32/ALU instructions
-        f = (clk.get("sm_mhz") or peaks["sm_max_mhz"]) * 1e6
-        peak_ops = 148 * 128 * f
-        roof["composite"] = {"bound": "alu", "evaluated_pairs_per_s": eval_per_s, "fragments_per_s": frag_per_s,
-                             "ms_per_step": st_ms["composite"], "sm_clock_hz": f, "peak_lane_ops_per_s": peak_ops}
+    # Rooflines: the dominant kernel of the step is
+    # K6 (composite), bound by FP32/ALU issue; its algorithmic work is SURVEY
+    # §8(d)'s 28 ops per evaluated (pixel, entry) pair of the plain definition +
+    # 8 per blended fragment.  The key sort (K4b tile sort) is reported against
+    # HBM, as the north_star asks.  Both use device times from CUDA events
+    # bracketing those kernels on their launch stream inside the timed region.
+    f_clk = (clk.get("sm_mhz") or peaks["sm_max_mhz"]) * 1e6
+    peak_ops = 148 * 128 * f_clk / 1e12  # FP32 lanes x clock, Top/s
+    traffic = load_traffic()
+    comp_ops = (28.0 * frags[1] + 8.0 * frags[0]) / args.steps  # per step
+    comp_t = st_ms["composite"] / 1e3
+    ach_ops = comp_ops / comp_t / 1e12
+    n_comp = max(1, stages["composite"]["launches"] // args.steps)
+    roof = {"bound": "alu", "kernel": "k6_composite_v2", "achieved": round(ach_ops, 2), "peak": round(peak_ops, 2),
+            "unit": "Top/s", "frac": round(ach_ops / peak_ops, 4),
+            "traffic": traffic.get("k6_composite_v2"),
+            "work": "28 FP32 ops per (pixel, list entry) pair the plain definition evaluates + 8 per blended "
+                    "fragment, per launch = 16 views",
+            "peak_source": f"148 SMs x 128 FP32 lanes x {f_clk / 1e6:.0f} MHz (median SM clock under load)",
+            "share_of_step": round(st_ms["composite"] / sum(st_ms.values()), 3),
+            "launches_per_step": n_comp}
+    ach_sort = st_by["tile_sort"] / (st_ms["tile_sort"] / 1e3) / 1e9
+    roof_sort = {"bound": "hbm", "kernel": "tile_sort (K4b onesweep passes)", "achieved": round(ach_sort, 1),
+                 "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": round(ach_sort / peaks["hbm_gbs"], 4),
+                 "traffic": traffic.get("tile_sort"),
+                 "peak_source": peaks["source"] + " hbm_gbs (MEASURED_PEAKS.json)",
+                 "share_of_step": round(st_ms["tile_sort"] / sum(st_ms.values()), 3)}
 
     line = {"metric": METRIC, "value": round(views_per_s, 2), "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 3),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (seeded generator of BASELINE.json configs[2]; no dataset)",
             "config": cfg_json, "fragments_per_sec": frag_per_s, "evaluated_pairs_per_sec": eval_per_s,
-            "wall_ms_per_step": round(wall_ms / args.steps, 3), "roofline": roof, "stages": stage_tab,
+            "wall_ms_per_step": round(wall_ms / args.steps, 3), "roofline": roof, "roofline_sort": roof_sort,
+            "stages": stage_tab,
             "gpu_launches": int(launches * world), "clocks": clk, "e2e": e2e,
             "keys_per_step_rank0": int(sum(scorer.last_keys))}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
