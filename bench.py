@@ -112,7 +112,9 @@ class ClockSampler:
 def run_reference(args, scene, cfg_json):
     import oracle
     n_threads = os.cpu_count() or 1
-    nv = args.cpu_views or max(8, min(32, 2 * n_threads))
+    # one view per host thread per step (~16 s of wall time on the GPU box), so
+    # the whole --steps K --warmup W run stays within a few minutes
+    nv = args.cpu_views or max(4, min(32, n_threads))
     idx = np.linspace(0, len(scene.cameras) - 1, nv).round().astype(np.int64)
     cams = np.ascontiguousarray(scene.cameras[idx])
     oracle.build()
@@ -143,7 +145,7 @@ def run_reference(args, scene, cfg_json):
 def cpu_baseline(scene, n_views: int):
     import oracle
     n_threads = os.cpu_count() or 1
-    nv = n_views or max(8, min(32, 2 * n_threads))
+    nv = n_views or max(4, min(32, n_threads))
     idx = np.linspace(0, len(scene.cameras) - 1, nv).round().astype(np.int64)
     cams = np.ascontiguousarray(scene.cameras[idx])
     oracle.build()

@@ -19,7 +19,7 @@ PROF = os.path.join(ROOT, "profiles")
 
 
 def short(name: str) -> str:
-    n = name.replace("gsr::", "").replace("(anonymous namespace)::", "").replace("<unnamed>::", "")
+    n = name.replace("CUtensorMap_st, ", "").replace("void ", "").replace("gsr::", "").replace("(anonymous namespace)::", "").replace("<unnamed>::", "")
     n = n.replace("unnamed>::", "")
     for sep in ("(const", "(float", "(unsigned", "(long", "(int"):
         if sep in n:
