@@ -43,6 +43,7 @@ def parse():
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="gsr", choices=["gsr", "reference"])
     p.add_argument("--batch-views", type=int, default=16)
+    p.add_argument("--slots", type=int, default=2, help="concurrent batch pipelines (streams)")
     p.add_argument("--cpu-views", type=int, default=0, help="oracle sample size (0 = auto)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
@@ -166,7 +167,8 @@ def main():
     import synth
     cfg_json = {"workload": synth.CONFIG_NAMES[CONFIG_ID], "gaussians": 1_000_000, "sh_degree": 3,
                 "views": 1024, "width": 800, "height": 800, "focal_px": 900, "tile": 16,
-                "batch_views": args.batch_views, "parallelism": f"dp{world} (views v mod N)",
+                "batch_views": args.batch_views, "streams": args.slots,
+                "parallelism": f"dp{world} (views v mod N)",
                 "l2": "inputs larger than L2: 240 MB field + ~0.9 GB keys per 16-view batch, no flush"}
 
     if args.impl == "reference":
@@ -196,8 +198,7 @@ def main():
     planes = torch.empty((P, n, 4), dtype=torch.float32, device=dev)
     planes.copy_(host_planes, non_blocking=False)
     G = Gaussians(planes, 3)
-    scorer = ViewScorer(G, batch_views=args.batch_views)
-    ctx = scorer.ctx
+    scorer = ViewScorer(G, batch_views=args.batch_views, n_slots=args.slots)
 
     def score_fn(c):
         return scorer.score_views(c)
@@ -221,9 +222,9 @@ def main():
         torch.cuda.synchronize()
 
     def timed(k, e2e=False, stage_timing=False):
-        ctx.timing(stage_timing)
-        ctx.timing_read()
-        scorer.n_frag.zero_()
+        scorer.timing(stage_timing)
+        scorer.timing_read()
+        scorer.reset_counters()
         barrier()
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         t0 = time.perf_counter()
@@ -234,8 +235,8 @@ def main():
         barrier()
         wall = time.perf_counter() - t0
         ms = ev0.elapsed_time(ev1)
-        stages = ctx.timing_read()
-        ctx.timing(False)
+        stages = scorer.timing_read()
+        scorer.timing(False)
         t = torch.tensor([ms, wall * 1e3], dtype=torch.float64, device=dev)
         fr = scorer.n_frag.clone().to(torch.float64)
         if world > 1:

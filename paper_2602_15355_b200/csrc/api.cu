@@ -80,6 +80,8 @@ gsr_status gsr_create(gsr_ctx** out, int device) {
   cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
   if (const char* v = std::getenv("GSR_COMPOSITE")) c->composite_variant = std::atoi(v);
   if (const char* v = std::getenv("GSR_SORT")) c->sort_variant = std::atoi(v);
+  if (const char* v = std::getenv("GSR_STAGES")) c->composite_stages = std::atoi(v);
+  if (const char* v = std::getenv("GSR_PIX")) c->composite_pix = std::atoi(v);
   e = cudaMallocHost(&c->host_pinned, 4096);
   if (e != cudaSuccess) {
     delete c;

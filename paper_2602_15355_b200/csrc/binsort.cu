@@ -945,8 +945,8 @@ constexpr int PKPT32 = 12; // persistent onesweep u32 keys: 3072 keys per tile
 constexpr int KPT32 = 12;  // onesweep u32 keys: 3072 keys per block
 
 // Sort-pass variants (gsr_ctx::sort_variant, env GSR_SORT):
-//   1  onesweep, one tile per block, decoupled look-back
-//   2  persistent onesweep, TMA-fed double buffer, windowed look-back (default)
+//   1  onesweep, one tile per block, decoupled look-back (default: best with 2 streams)
+//   2  persistent onesweep, TMA-fed double buffer, windowed look-back
 //   3  reduce-then-scan: rs_upsweep + rs_scan + onesweep<LB=1> scatter
 template <typename KeyT>
 size_t pass_tile(int variant) {

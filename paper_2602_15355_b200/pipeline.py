@@ -1,19 +1,25 @@
 """Host orchestration of one scoring pass (Alg. 1 L147-154 body): for every
 candidate view, K1 project -> K2..K5 bin+sort -> K6 composite -> K7 score,
 batched by view; then K8 top-k.  All arithmetic runs in libgsr's kernels;
-this file only sizes buffers and sequences the C-ABI calls on one stream.
+this file only sizes buffers and sequences the C-ABI calls.
+
+Batches alternate between ``n_slots`` independent slots, each with its own
+CUDA stream, gsr context (scratch) and pipeline buffers, so the GPU runs
+batch b's compositing (FP32-issue bound) concurrently with batch b+1's
+projection and sorts (memory / latency bound): the two kinds of kernels
+share the SMs instead of idling them in turn.
 """
 from __future__ import annotations
 
 import math
 from dataclasses import dataclass
-from typing import Optional
+from typing import List, Optional
 
 import numpy as np
 import torch
 
 from . import gsr
-from .gsr import CAM_DTYPE, Context, Gaussians, GsrError
+from .gsr import Context, Gaussians, GsrError
 
 
 def tiles_per_view(cam) -> int:
@@ -27,87 +33,165 @@ class BatchOut:
     images: Optional[torch.Tensor] = None  # [V][H][W][4]
 
 
-class ViewScorer:
-    """Scores candidate views of one Gaussian field on one GPU.
+class _Slot:
+    """One batch pipeline: K1..K5 on a high-priority stream (`stream`), K6/K7
+    on a low-priority stream (`comp`) that waits for the sort; the next use of
+    the slot waits for the previous composite.  With two slots the block
+    scheduler fills the SMs left idle by the (latency-bound) sorts with
+    compositing blocks of the previous batch."""
 
-    ``batch_views`` views share one K1 launch (the parameter planes are read
-    once per batch) and one pair of sorts.  Buffers grow on demand; the key
-    capacity follows the capacity protocol of gsr_bin_sort (GSR_ECAPACITY
-    returns the required size, we grow by 25% and retry)."""
-
-    def __init__(self, field: Gaussians, batch_views: int = 8, ctx: Optional[Context] = None,
-                 stream: Optional[torch.cuda.Stream] = None):
-        self.field = field
-        self.dev = field.planes.device
-        self.ctx = ctx or Context(self.dev.index or 0)
-        self.V = min(int(batch_views), gsr.GSR_MAX_VIEWS)
+    def __init__(self, dev, V: int, n: int, stream, comp=None):
+        self.ctx = Context(dev.index or 0)
         self.stream = stream
-        n = field.n
-        self.rec = torch.empty((self.V, max(n, 1), 12), dtype=torch.float32, device=self.dev)
-        self.bin = torch.empty((4, self.V, max(n, 1)), dtype=torch.int32, device=self.dev)
+        self.comp = comp if comp is not None else stream
+        with torch.cuda.stream(stream):
+            self.rec = torch.empty((V, max(n, 1), 12), dtype=torch.float32, device=dev)
+            self.bin = torch.empty((4, V, max(n, 1)), dtype=torch.int32, device=dev)
+            self.n_frag = torch.zeros(2, dtype=torch.int64, device=dev)  # [blended, evaluated]
         self.capacity = 0
         self.vals = None
         self.keys = None
         self.ranges = None
         self.partial = None
-        self.n_frag = torch.zeros(2, dtype=torch.int64, device=self.dev)  # [blended, evaluated]
-        self.last_keys = []
 
-    def _ensure_keys(self, cap: int, want_keys: bool):
-        if cap > self.capacity or (want_keys and self.keys is None):
-            self.capacity = max(cap, self.capacity)
-            self.vals = torch.empty(max(self.capacity, 1), dtype=torch.int32, device=self.dev)
-            self.keys = torch.empty(max(self.capacity, 1), dtype=torch.int64, device=self.dev) if want_keys else None
 
-    def _ensure_tiles(self, T: int):
-        if self.ranges is None or self.ranges.shape[0] < T:
-            self.ranges = torch.empty((T, 2), dtype=torch.int32, device=self.dev)
-            self.partial = torch.empty(T, dtype=torch.float32, device=self.dev)
+class ViewScorer:
+    """Scores candidate views of one Gaussian field on one GPU.
 
+    ``batch_views`` views share one K1 launch (the parameter planes are read
+    once per batch) and one pair of sorts.  Buffers grow on demand; the key
+    capacity follows gsr_bin_sort's capacity protocol (GSR_ECAPACITY returns
+    the required size; grow by 25 % and retry)."""
+
+    def __init__(self, field: Gaussians, batch_views: int = 16, n_slots: int = 2):
+        self.field = field
+        self.dev = field.planes.device
+        self.V = min(int(batch_views), gsr.GSR_MAX_VIEWS)
+        self.slots: List[_Slot] = []
+        lo, hi = torch.cuda.Stream.priority_range() if hasattr(torch.cuda.Stream, "priority_range") else (0, -1)
+        for _ in range(max(1, n_slots)):
+            if n_slots > 1:
+                self.slots.append(_Slot(self.dev, self.V, field.n, torch.cuda.Stream(self.dev, priority=hi),
+                                        torch.cuda.Stream(self.dev, priority=lo)))
+            else:
+                self.slots.append(_Slot(self.dev, self.V, field.n, torch.cuda.Stream(self.dev)))
+        self.ctx = self.slots[0].ctx
+        self.last_keys: List[int] = []
+
+    # ------------------------------------------------------------------ helpers
+    @property
+    def n_frag(self) -> torch.Tensor:
+        """[blended fragments, evaluated pairs] summed over slots (device)."""
+        return torch.stack([s.n_frag for s in self.slots]).sum(0)
+
+    def reset_counters(self):
+        for s in self.slots:
+            s.n_frag.zero_()
+
+    def timing(self, enable: bool = True):
+        for s in self.slots:
+            s.ctx.timing(enable)
+
+    def timing_read(self) -> dict:
+        acc = None
+        for s in self.slots:
+            t = s.ctx.timing_read()
+            if acc is None:
+                acc = t
+            else:
+                for k, v in t.items():
+                    for f in v:
+                        acc[k][f] += v[f]
+        return acc
+
+    # Slot buffers are allocated with the slot's stream current, so the caching
+    # allocator only recycles them in that stream's order (a replaced buffer may
+    # still be read by the slot's previous, not yet finished, composite).
+    @staticmethod
+    def _ensure_keys(slot: _Slot, cap: int, want_keys: bool):
+        if cap > slot.capacity or (want_keys and slot.keys is None):
+            slot.capacity = max(cap, slot.capacity)
+            with torch.cuda.stream(slot.stream):
+                slot.vals = torch.empty(max(slot.capacity, 1), dtype=torch.int32, device=slot.rec.device)
+                slot.keys = (torch.empty(max(slot.capacity, 1), dtype=torch.int64, device=slot.rec.device)
+                             if want_keys else None)
+
+    @staticmethod
+    def _ensure_tiles(slot: _Slot, T: int):
+        if slot.ranges is None or slot.ranges.shape[0] < T:
+            with torch.cuda.stream(slot.stream):
+                slot.ranges = torch.empty((T, 2), dtype=torch.int32, device=slot.rec.device)
+                slot.partial = torch.empty(T, dtype=torch.float32, device=slot.rec.device)
+
+    # ------------------------------------------------------------------ batches
     def run_batch(self, cams: np.ndarray, scores_out: torch.Tensor, images: Optional[torch.Tensor] = None,
-                  t_final=None, n_contrib=None, want_keys: bool = False) -> BatchOut:
-        """Score len(cams) <= batch_views same-resolution views into scores_out[0:len(cams)]."""
+                  t_final=None, n_contrib=None, want_keys: bool = False, slot: int = 0) -> BatchOut:
+        """Score len(cams) <= batch_views same-resolution views into
+        scores_out[0:len(cams)], enqueued on the slot's stream.  Standalone
+        calls are ordered after, and joined back into, the caller's stream."""
+        caller = torch.cuda.current_stream(self.dev)
+        S = self.slots[slot]
+        S.stream.wait_stream(caller)
+        S.comp.wait_stream(caller)
+        out = self._enqueue(S, cams, scores_out, images, t_final, n_contrib, want_keys)
+        caller.wait_stream(S.comp)
+        return out
+
+    def _enqueue(self, S: _Slot, cams, scores_out, images=None, t_final=None, n_contrib=None,
+                 want_keys: bool = False) -> BatchOut:
         cams = gsr.cams_array(cams)
         V = len(cams)
         assert 0 < V <= self.V
         n = self.field.n
-        tpv = tiles_per_view(cams[0])
-        self._ensure_tiles(V * tpv)
-        if self.capacity == 0:
-            self._ensure_keys(max(1 << 20, 4 * n * V), want_keys)
+        self._ensure_tiles(S, V * tiles_per_view(cams[0]))
+        if S.capacity == 0:
+            self._ensure_keys(S, max(1 << 20, 4 * n * V), want_keys)
         elif want_keys:
-            self._ensure_keys(self.capacity, True)
-        st = self.stream
-        gsr.gsr_project(self.ctx, self.field, cams, self.rec, self.bin, st)
+            self._ensure_keys(S, S.capacity, True)
+        st = S.stream
+        if S.comp is not S.stream:
+            st.wait_stream(S.comp)  # the previous composite of this slot still reads rec / vals / ranges
         # rec / bin hold [V][n][12] and [4][V][n] for THIS batch's V, packed from the
-        # start of the (batch_views-sized) buffers: pass the base pointers.
+        # start of the (batch_views-sized) buffers: the base pointers are passed.
+        gsr.gsr_project(S.ctx, self.field, cams, S.rec, S.bin, st)
         while True:
             try:
-                K = gsr.gsr_bin_sort(self.ctx, self.bin, n, cams, self.vals, self.capacity, self.ranges,
-                                     keys=self.keys if want_keys else None, stream=st)
+                K = gsr.gsr_bin_sort(S.ctx, S.bin, n, cams, S.vals, S.capacity, S.ranges,
+                                     keys=S.keys if want_keys else None, stream=st)
                 break
             except GsrError as e:
                 if e.status != gsr.GSR_ECAPACITY:
                     raise
-                self._ensure_keys(int(math.ceil(e.required * 1.25)) + 1024, want_keys)
-        gsr.gsr_composite(self.ctx, self.rec, n, self.vals, self.ranges, cams, self.partial, rgbu=images,
-                          t_final=t_final, n_contrib=n_contrib, n_frag=self.n_frag, stream=st)
-        gsr.gsr_score_views(self.ctx, self.partial, cams, scores_out, st)
+                self._ensure_keys(S, int(math.ceil(e.required * 1.25)) + 1024, want_keys)
+        cs = S.comp
+        if cs is not st:
+            cs.wait_stream(st)
+        gsr.gsr_composite(S.ctx, S.rec, n, S.vals, S.ranges, cams, S.partial, rgbu=images, t_final=t_final,
+                          n_contrib=n_contrib, n_frag=S.n_frag, stream=cs)
+        gsr.gsr_score_views(S.ctx, S.partial, cams, scores_out, cs)
         return BatchOut(K, images)
 
     def score_views(self, cams: np.ndarray, scores_out: Optional[torch.Tensor] = None) -> torch.Tensor:
-        """Scores for all of ``cams`` (any count; same resolution), batched."""
+        """Scores for all of ``cams`` (any count; same resolution), batches
+        alternating over the slots' streams; the result is ordered back onto
+        the caller's current stream."""
         cams = gsr.cams_array(cams)
         if scores_out is None:
             scores_out = torch.empty(len(cams), dtype=torch.float32, device=self.dev)
+        caller = torch.cuda.current_stream(self.dev)
+        for s in self.slots:
+            s.stream.wait_stream(caller)  # inputs (field, scores_out) produced on the caller's stream
+            s.comp.wait_stream(caller)
         self.last_keys = []
-        for b0 in range(0, len(cams), self.V):
+        for i, b0 in enumerate(range(0, len(cams), self.V)):
             b1 = min(len(cams), b0 + self.V)
-            out = self.run_batch(cams[b0:b1], scores_out[b0:b1])
+            out = self._enqueue(self.slots[i % len(self.slots)], cams[b0:b1], scores_out[b0:b1])
             self.last_keys.append(out.n_keys)
+        for s in self.slots:
+            caller.wait_stream(s.comp)
         return scores_out
 
     def select(self, scores: torch.Tensor, k: int = 1, exclude=None) -> torch.Tensor:
         out = torch.empty(k, dtype=torch.int32, device=self.dev)
-        gsr.gsr_select_nbv(self.ctx, scores, k, out, exclude, self.stream)
+        gsr.gsr_select_nbv(self.ctx, scores, k, out, exclude, torch.cuda.current_stream(self.dev))
         return out
