@@ -268,11 +268,12 @@ __global__ void __launch_bounds__(256, 3) onesweep(const KeyT* __restrict__ kin,
     Stage st;
   };
   __shared__ Smem u;
-  __shared__ uint32_t s_start[256], s_gbase[256], s_wsum[W];
+  __shared__ uint32_t s_start[256], s_gbase[256], s_cnt[256], s_wsum[W];
   __shared__ uint32_t s_bid;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (tid == 0) s_bid = LB ? blockIdx.x : atomicAdd(ctr, 1u);
   for (int i = tid; i < W * 256; i += B) (&u.hist[0][0])[i] = 0;
+  s_cnt[tid] = 0;
   __syncthreads();
   const uint32_t bid = s_bid;
   const uint32_t mask = (nbits >= 32) ? 0xffffffffu : ((1u << nbits) - 1);
@@ -288,6 +289,26 @@ __global__ void __launch_bounds__(256, 3) onesweep(const KeyT* __restrict__ kin,
     key[k] = valid ? kin[idx] : KeyT(0);
   }
   const uint32_t lt = (1u << lane) - 1;
+  // Early digit counts (shared atomics): the tile's aggregate is published and
+  // the first window of look-back loads is in flight while the warps rank.
+  constexpr int WIN = 8;
+  uint32_t win[WIN];
+  uint32_t early_total = 0;
+  if (!LB) {
+#pragma unroll
+    for (int k = 0; k < KPT; ++k) {
+      const int64_t idx = wbase + k * 32 + lane;
+      if (idx < (int64_t)n) atomicAdd(&s_cnt[(uint32_t)(key[k] >> shift) & mask], 1u);
+    }
+    __syncthreads();
+    early_total = s_cnt[tid];
+    st_word(lookback + (size_t)bid * 256 + tid, (bid == 0 ? DG_INC : DG_AGG) | early_total);
+#pragma unroll
+    for (int i = 0; i < WIN; ++i) {
+      const int64_t j = (int64_t)bid - 1 - i;
+      win[i] = j >= 0 ? ld_word(lookback + (size_t)j * 256 + tid) : DG_INC;
+    }
+  }
 #pragma unroll
   for (int k = 0; k < KPT; ++k) {
     const int64_t idx = wbase + k * 32 + lane;
@@ -317,24 +338,35 @@ __global__ void __launch_bounds__(256, 3) onesweep(const KeyT* __restrict__ kin,
     uint32_t excl = 0;
     if (LB) {
       excl = lookback[(size_t)d * gridDim.x + bid] - base[d];  // gofs - digit base
-    } else if (bid == 0) {
-      st_word(my, DG_INC | total);
-    } else {
-      st_word(my, DG_AGG | total);
+    } else if (bid != 0) {
+      // windowed decoupled look-back: WIN predecessors per round trip
       int64_t j = (int64_t)bid - 1;
       while (true) {
+        int i = 0;
+        bool done = false;
+#pragma unroll
+        for (; i < WIN; ++i) {
+          const uint32_t f = win[i] >> 30;
+          if (f == 0) break;
+          excl += win[i] & DG_VAL;
+          if (f == 2) {
+            done = true;
+            break;
+          }
+        }
+        if (done) break;
+        j -= i;  // consumed i aggregates; re-read from the first word not yet ready
 #ifdef GSR_DEBUG
         if (j < 0) {
           printf("onesweep lookback underflow bid=%u d=%d n=%u shift=%d\n", bid, d, n, shift);
           __trap();
         }
 #endif
-        const uint32_t w = ld_word(lookback + (size_t)j * 256 + d);
-        const uint32_t f = w >> 30;
-        if (f == 0) continue;
-        excl += w & DG_VAL;
-        if (f == 2) break;
-        --j;
+#pragma unroll
+        for (int q = 0; q < WIN; ++q) {
+          const int64_t jj = j - q;
+          win[q] = jj >= 0 ? ld_word(lookback + (size_t)jj * 256 + d) : DG_INC;
+        }
       }
       st_word(my, DG_INC | (excl + total));
     }
@@ -752,7 +784,7 @@ __global__ void __launch_bounds__(256) k3_emit(const uint64_t* __restrict__ dkey
   __syncthreads();
   const int64_t bid = s_bid;
   const uint32_t view0 = s_view0;
-  const uint32_t lo = view0 * tpv, hi = lo + (uint32_t)smem_bins;
+  const uint32_t lo = view0 * tpv;
   const int64_t e0 = bid * K3_TILE + (int64_t)warp * (32 * K3_ROUNDS);
   uint32_t nt[K3_ROUNDS], xr[K3_ROUNDS], yr[K3_ROUNDS], g[K3_ROUNDS], view[K3_ROUNDS];
   uint64_t mine = 0;
@@ -813,24 +845,28 @@ __global__ void __launch_bounds__(256) k3_emit(const uint64_t* __restrict__ dkey
       const uint32_t okb = __shfl_sync(FULL, kbase, s), ow = __shfl_sync(FULL, wdt, s);
       const float orcp = __shfl_sync(FULL, rcp, s);
       const uint32_t og = __shfl_sync(FULL, g[r], s);
-      const bool act = j < total;
-      uint32_t key = 0xffffffffu;
-      if (act) {
+      if (j < total) {
         const uint32_t loc = j - oexcl;
-        uint32_t q = (uint32_t)((float)loc * orcp);  // loc < 2^24: off by at most one
-        int32_t rem = (int32_t)(loc - q * ow);
-        if (rem >= (int32_t)ow) { ++q; rem -= ow; }
-        if (rem < 0) { --q; rem += ow; }
-        key = okb + q * gx + (uint32_t)rem;
+        uint32_t q = __float2uint_rz((float)loc * orcp);  // loc < 2^24: off by at most one
+        uint32_t rem = loc - q * ow;
+        if ((int32_t)rem < 0) {
+          --q;
+          rem += ow;
+        } else if (rem >= ow) {
+          ++q;
+          rem -= ow;
+        }
+        const uint32_t key = okb + q * gx + rem;
         tkeys[base + j] = key;
         tvals[base + j] = og;
-      }
-      const uint32_t peers = __match_any_sync(FULL, key);
-      if (act && (__ffs(peers) - 1) == lane) {
-        if (key >= lo && key < hi)
-          atomicAdd(s_cnt + (key - lo), (uint32_t)__popc(peers));
+        // Tile counts: shared-memory histogram of the block's view (aggregated
+        // per block, flushed with one global atomic per non-empty bin).  A
+        // MATCH.ANY warp aggregation was measured to cost more than it saved:
+        // keys of one 32-key window are almost always distinct tiles.
+        if (key - lo < (uint32_t)smem_bins)
+          atomicAdd(s_cnt + (key - lo), 1u);
         else
-          atomicAdd(counts + key, (uint32_t)__popc(peers));
+          atomicAdd(counts + key, 1u);
       }
     }
     base += total;

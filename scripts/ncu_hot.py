@@ -3,6 +3,7 @@ import csv
 import sys
 
 path, top = sys.argv[1], int(sys.argv[2]) if len(sys.argv) > 2 else 30
+which = sys.argv[3] if len(sys.argv) > 3 else None  # substring of the kernel name
 rows = list(csv.reader(open(path)))
 # the file may hold several kernels: split at "Kernel Name" rows
 blocks, cur = [], None
@@ -12,7 +13,8 @@ for r in rows:
         blocks.append(cur)
     elif cur is not None:
         cur["rows"].append(r)
-for b in blocks[:1]:
+sel = [b for b in blocks if which is None or which in b["name"]][:1]
+for b in sel:
     hdr, data = b["rows"][0], b["rows"][1:]
     i_src, i_s = hdr.index("Source"), hdr.index("Warp Stall Sampling (All Samples)")
     i_e, i_t = hdr.index("Instructions Executed"), hdr.index("Avg. Threads Executed")
