@@ -252,7 +252,7 @@ __global__ void __launch_bounds__(256) hist_u64(const uint64_t* __restrict__ key
 //         precomputed by rs_upsweep + rs_scan (lookback = gofs[256][ntiles]),
 //         so a tile needs no inter-block communication at all.
 template <typename KeyT, int KPT, int MODE, int LB = 0>
-__global__ void __launch_bounds__(256, 3) onesweep(const KeyT* __restrict__ kin, const uint32_t* __restrict__ vin,
+__global__ void __launch_bounds__(256, (KPT <= 8 ? 4 : 3)) onesweep(const KeyT* __restrict__ kin, const uint32_t* __restrict__ vin,
                                                 KeyT* __restrict__ kout, uint32_t* __restrict__ vout, uint32_t n,
                                                 int shift, int nbits, const uint32_t* __restrict__ base,
                                                 uint32_t* __restrict__ lookback, uint32_t* __restrict__ ctr,
@@ -985,25 +985,16 @@ constexpr int KPT32 = 12;  // onesweep u32 keys: 3072 keys per block
 //   2  persistent onesweep, TMA-fed double buffer, windowed look-back
 //   3  reduce-then-scan: rs_upsweep + rs_scan + onesweep<LB=1> scatter
 template <typename KeyT>
-size_t pass_tile(int variant) {
+size_t pass_tile(int variant, int kpt32 = KPT32) {
   if (variant == 2) return 256 * (sizeof(KeyT) == 8 ? PKPT64 : PKPT32);
-  return 256 * (sizeof(KeyT) == 8 ? KPT64 : KPT32);
+  return 256 * (sizeof(KeyT) == 8 ? KPT64 : kpt32);
 }
 
-// One stable LSD pass by digit (key >> shift) & (2^nbits - 1).  `region` holds
-// ceil(n / pass_tile) * 256 zero-initialised words (look-back flags or the
-// per-(digit, tile) offsets); `ctr` one zero-initialised counter.
-template <typename KeyT, int MODE>
-cudaError_t run_pass(int variant, int num_sms, const KeyT* kin, const uint32_t* vin, KeyT* kout, uint32_t* vout,
-                     uint32_t n, int shift, int nbits, const uint32_t* base, uint32_t* region, uint32_t* ctr,
-                     uint64_t* keys64, const uint32_t* depth_plane, uint32_t tpv, int64_t nper, cudaStream_t st) {
-  if (n == 0) return cudaSuccess;
-  constexpr int K = sizeof(KeyT) == 8 ? KPT64 : KPT32;
-  constexpr int PK = sizeof(KeyT) == 8 ? PKPT64 : PKPT32;
-  const uint32_t nt = (uint32_t)((n + pass_tile<KeyT>(variant) - 1) / pass_tile<KeyT>(variant));
-  if (variant == 2)
-    return launch_pass<KeyT, PK, MODE>(kin, vin, kout, vout, n, shift, nbits, base, region, ctr, keys64, depth_plane,
-                                       tpv, nper, num_sms, st);
+template <typename KeyT, int K, int MODE>
+cudaError_t launch_onesweep(int variant, uint32_t nt, const KeyT* kin, const uint32_t* vin, KeyT* kout,
+                            uint32_t* vout, uint32_t n, int shift, int nbits, const uint32_t* base, uint32_t* region,
+                            uint32_t* ctr, uint64_t* keys64, const uint32_t* depth_plane, uint32_t tpv, int64_t nper,
+                            cudaStream_t st) {
   if (variant == 1) {
     onesweep<KeyT, K, MODE, 0><<<nt, 256, 0, st>>>(kin, vin, kout, vout, n, shift, nbits, base, region, ctr, keys64,
                                                    depth_plane, tpv, nper);
@@ -1014,6 +1005,32 @@ cudaError_t run_pass(int variant, int num_sms, const KeyT* kin, const uint32_t* 
   onesweep<KeyT, K, MODE, 1><<<nt, 256, 0, st>>>(kin, vin, kout, vout, n, shift, nbits, base, region, ctr, keys64,
                                                  depth_plane, tpv, nper);
   return cudaGetLastError();
+}
+
+// One stable LSD pass by digit (key >> shift) & (2^nbits - 1).  `region` holds
+// ceil(n / pass_tile) * 256 zero-initialised words (look-back flags or the
+// per-(digit, tile) offsets); `ctr` one zero-initialised counter.
+template <typename KeyT, int MODE>
+cudaError_t run_pass(int variant, int num_sms, const KeyT* kin, const uint32_t* vin, KeyT* kout, uint32_t* vout,
+                     uint32_t n, int shift, int nbits, const uint32_t* base, uint32_t* region, uint32_t* ctr,
+                     uint64_t* keys64, const uint32_t* depth_plane, uint32_t tpv, int64_t nper, cudaStream_t st,
+                     int kpt32 = KPT32) {
+  if (n == 0) return cudaSuccess;
+  constexpr int PK = sizeof(KeyT) == 8 ? PKPT64 : PKPT32;
+  const uint32_t nt = (uint32_t)((n + pass_tile<KeyT>(variant, kpt32) - 1) / pass_tile<KeyT>(variant, kpt32));
+  if (variant == 2)
+    return launch_pass<KeyT, PK, MODE>(kin, vin, kout, vout, n, shift, nbits, base, region, ctr, keys64, depth_plane,
+                                       tpv, nper, num_sms, st);
+  if constexpr (sizeof(KeyT) == 8) {
+    return launch_onesweep<KeyT, KPT64, MODE>(variant, nt, kin, vin, kout, vout, n, shift, nbits, base, region, ctr,
+                                              keys64, depth_plane, tpv, nper, st);
+  } else {
+    if (kpt32 == 8)
+      return launch_onesweep<KeyT, 8, MODE>(variant, nt, kin, vin, kout, vout, n, shift, nbits, base, region, ctr,
+                                            keys64, depth_plane, tpv, nper, st);
+    return launch_onesweep<KeyT, KPT32, MODE>(variant, nt, kin, vin, kout, vout, n, shift, nbits, base, region, ctr,
+                                              keys64, depth_plane, tpv, nper, st);
+  }
 }
 inline int pass_launches(int variant) { return variant == 3 ? 3 : 1; }
 
@@ -1186,7 +1203,8 @@ extern "C" gsr_status gsr_bin_sort(gsr_ctx* ctx, const uint32_t* bin_rec, int64_
   tvb = (char*)tva + align_up(K * 4);
   if ((s = ensure(ctx, S_COUNTS, T * 4, &cnt)) != GSR_OK) return s;
   const int variant = ctx->sort_variant;
-  const size_t dtile = pass_tile<uint64_t>(variant), ttile = pass_tile<uint32_t>(variant);
+  const int kpt32 = ctx->sort_kpt32;
+  const size_t dtile = pass_tile<uint64_t>(variant), ttile = pass_tile<uint32_t>(variant, kpt32);
   const size_t nbd = (size_t)((nvis + dtile - 1) / dtile);
   const size_t nb3 = (size_t)((nvis + K3_TILE - 1) / K3_TILE);
   const size_t nbt = (size_t)((K + ttile - 1) / ttile);
@@ -1252,12 +1270,12 @@ extern "C" gsr_status gsr_bin_sort(gsr_ctx* ctx, const uint32_t* bin_rec, int64_
     cudaError_t e;
     if (p == tpasses - 1) {
       e = run_pass<uint32_t, 1>(variant, ctx->num_sms, tk, tv, nullptr, vals, (uint32_t)K, sh, nbits,
-                                tbase + 256 * p, lbp, ctrs + 6 + p, keys, p_depth, (uint32_t)tpv, n, st);
+                                tbase + 256 * p, lbp, ctrs + 6 + p, keys, p_depth, (uint32_t)tpv, n, st, kpt32);
     } else {
       uint32_t* ko = (p % 2 == 0) ? (uint32_t*)tkb : (uint32_t*)tka;
       uint32_t* vo = (p % 2 == 0) ? (uint32_t*)tvb : (uint32_t*)tva;
       e = run_pass<uint32_t, 0>(variant, ctx->num_sms, tk, tv, ko, vo, (uint32_t)K, sh, nbits, tbase + 256 * p, lbp,
-                                ctrs + 6 + p, nullptr, nullptr, 0, 0, st);
+                                ctrs + 6 + p, nullptr, nullptr, 0, 0, st, kpt32);
       tk = ko;
       tv = vo;
     }

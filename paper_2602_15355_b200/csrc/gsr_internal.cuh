@@ -82,6 +82,7 @@ struct gsr_ctx {
   int64_t launches[GSR_N_STAGES] = {};
   int64_t last_nvis = 0, last_keys = 0;  // of the last gsr_bin_sort (byte accounting)
   int sort_variant = 1;       // sort pass: 1 onesweep (default), 2 persistent onesweep, 3 reduce-then-scan (GSR_SORT)
+  int sort_kpt32 = 12;        // tile-sort keys per thread (GSR_KPT: 8 or 12)
   int composite_stages = 4;   // K6 ring depth (GSR_STAGES: 4 or 8)
   int composite_pix = 1;      // K6 pixels per consumer lane (GSR_PIX: 1 or 2)
   int composite_variant = 3;  // K6 loader: 1 block-sync LDG, 2 TMA bulk/record, 3 TMA gather4, 4 cp.async
