@@ -158,6 +158,32 @@ def cpu_baseline(scene, n_views: int):
                       f"{dt:.1f} s wall on {n_threads} threads", "fragments_per_sec": float(nf.sum()) / dt}
 
 
+def bench_w2(gsr, dev, peaks, reps: int = 20):
+    """NEXT-1: W2 latent scoring of N = 1000 candidates (M = 5, C = 4, 64 x 64;
+    PAPER.md L135, L181), HBM roofline on the 2 M C H W floats read per view."""
+    import torch
+    import synth
+    mu, s2 = synth.gen_latent_ensembles(1000, 5, 4, 64, 64, seed=0)
+    m, s = torch.from_numpy(mu).to(dev), torch.from_numpy(s2).to(dev)
+    sc = torch.empty(1000, device=dev)
+    ctx = gsr.Context(dev.index or 0)
+    for _ in range(3):
+        gsr.gsr_w2_scores(ctx, m, s, sc)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        gsr.gsr_w2_scores(ctx, m, s, sc)
+    e1.record()
+    torch.cuda.synchronize()
+    t = e0.elapsed_time(e1) / reps / 1e3
+    byts = 2.0 * mu.nbytes
+    return {"metric": "w2_candidates_scored_per_sec", "value": round(1000 / t, 1), "unit": "views/s",
+            "ms_per_pass": round(t * 1e3, 4), "config": "N=1000, M=5, C=4, 64x64 (synthetic latents)",
+            "roofline": {"bound": "hbm", "achieved": round(byts / t / 1e9, 1), "peak": peaks["hbm_gbs"],
+                         "unit": "GB/s", "frac": round(byts / t / 1e9 / peaks["hbm_gbs"], 4)}}
+
+
 # ----------------------------------------------------------------------------- GPU arm
 def main():
     args = parse()
@@ -311,6 +337,8 @@ def main():
             "stages": stage_tab,
             "gpu_launches": int(launches * world), "clocks": clk, "e2e": e2e,
             "keys_per_step_rank0": int(sum(scorer.last_keys))}
+    if rank == 0:
+        line["next1_w2"] = bench_w2(gsr, dev, peaks)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(scene, args.cpu_views)
     if rank == 0:

@@ -174,6 +174,18 @@ gsr_status gsr_score_views(gsr_ctx* ctx, const float* tile_partial, const gsr_ca
 gsr_status gsr_select_nbv(gsr_ctx* ctx, const float* scores, int32_t n, const uint8_t* exclude,
                           int32_t k, int32_t* out_idx, void* stream);
 
+/* ---- NEXT-1: latent-space ensemble disagreement (PAPER.md eq:w2_pixel,
+   §3.3) ---------------------------------------------------------------
+   For each candidate view v: W2 = (1/(H_z W_z)) sum_p (1/C(M,2)) sum_{i<j}
+   ( ||mu_{i,p} - mu_{j,p}||^2 + sum_c (s2_{i,p,c} + s2_{j,p,c} - 2 sqrt(s2_{i,p,c} s2_{j,p,c})) ),
+   each sample m a diagonal-Gaussian latent (mean mu, per-channel variance s2).
+   mu, s2   [V][M][C][HW] float (device), s2 >= 0
+   scores   [V] float;  map OPTIONAL [V][HW] float per-location divergence
+   EINVAL unless V >= 1, M >= 2, C >= 1, HW >= 1.  The LPIPS term of
+   eq:uncert_latent is not part of this call (no pretrained network). */
+gsr_status gsr_w2_scores(gsr_ctx* ctx, const float* mu, const float* s2, int32_t n_views, int32_t M, int32_t C,
+                         int64_t HW, float* scores, float* map, void* stream);
+
 /* ---- utility: the onesweep LSD radix sort used by gsr_bin_sort ------------
    Stable sort of (key, value) pairs by key bits [begin_bit, end_bit), 8-bit
    digits, one upfront histogram pass + one decoupled-lookback scatter pass
@@ -200,7 +212,8 @@ enum {
   GSR_STAGE_SCORE = 7,      /* K7 */
   GSR_STAGE_SELECT = 8,     /* K8 */
   GSR_STAGE_SORT_U64 = 9,   /* utility sort (histogram + passes) */
-  GSR_N_STAGES = 10
+  GSR_STAGE_W2 = 10,        /* NEXT-1 latent W2 scorer */
+  GSR_N_STAGES = 11
 };
 /* enable != 0: bracket every stage with CUDA events on its launch stream. */
 gsr_status gsr_timing_enable(gsr_ctx* ctx, int enable);

@@ -58,6 +58,7 @@ enum Slot {
   S_TOTALS,                                 // device totals (Nvis, K)
   S_SORTK, S_SORTV,                         // utility sort ping-pong
   S_SELECT,                                 // exclusion mask staging
+  S_SELECT2,                                // NEXT-1 per-chunk partial sums
   S_NSLOTS
 };
 

@@ -31,9 +31,9 @@ assert CAM_DTYPE.itemsize == 96
 
 EXPORTED = ["gsr_create", "gsr_destroy", "gsr_last_error", "gsr_version", "gsr_camera_look_at",
             "gsr_project", "gsr_bin_sort", "gsr_composite", "gsr_score_views", "gsr_select_nbv",
-            "gsr_sort_pairs_u64", "gsr_scratch_bytes", "gsr_timing_enable", "gsr_timing_read"]
+            "gsr_sort_pairs_u64", "gsr_scratch_bytes", "gsr_timing_enable", "gsr_timing_read", "gsr_w2_scores"]
 STAGES = ["project", "compact", "depth_sort", "emit", "ranges", "tile_sort", "composite", "score", "select",
-          "sort_u64"]
+          "sort_u64", "w2"]
 
 
 class GsrError(RuntimeError):
@@ -66,6 +66,7 @@ def _load():
     L.gsr_score_views.argtypes = [P, P, P, i32, P, P]
     L.gsr_select_nbv.argtypes = [P, P, i32, P, i32, P, P]
     L.gsr_sort_pairs_u64.argtypes = [P, P, P, P, P, i64, i32, i32, P]
+    L.gsr_w2_scores.argtypes = [P, P, P, i32, i32, i32, i64, P, P, P]
     L.gsr_timing_enable.argtypes = [P, ctypes.c_int]
     L.gsr_timing_read.argtypes = [P, P, P, P]
     L.gsr_scratch_bytes.argtypes = [P]
@@ -222,3 +223,11 @@ def gsr_sort_pairs_u64(ctx: Context, keys_in, vals_in, keys_out, vals_out, begin
                        stream=None):
     ctx._check(lib.gsr_sort_pairs_u64(ctx.handle, _ptr(keys_in), _ptr(vals_in), _ptr(keys_out), _ptr(vals_out),
                                       int(keys_in.numel()), begin_bit, end_bit, _stream(stream)))
+
+
+def gsr_w2_scores(ctx: Context, mu, s2, scores, map_out=None, stream=None):
+    """NEXT-1 (PAPER.md eq:w2_pixel): mu, s2 CUDA float tensors [V][M][C][HW]."""
+    V, M, C, HW = (int(x) for x in mu.shape)
+    assert tuple(s2.shape) == (V, M, C, HW) and mu.is_contiguous() and s2.is_contiguous()
+    ctx._check(lib.gsr_w2_scores(ctx.handle, _ptr(mu), _ptr(s2), V, M, C, HW, _ptr(scores), _ptr(map_out),
+                                 _stream(stream)))

@@ -357,3 +357,20 @@ def random_scene_small(seed: int, n: int, width: int = 48, height: int = 40, foc
     fld = pack_field(means, scales, q, opac, sh, unc, sh_degree)
     cams = fibonacci_cameras(n_views, 3.0, width, height, focal)
     return fld, cams
+
+
+# --------------------------------------------------------------------------
+# NEXT-1: synthetic diffusion-latent ensembles (VAE
+# latents 4 x 64 x 64, M = 5 stochastic passes).  The pretrained prior is not
+# available; each candidate view gets a base latent mean, per-sample
+# perturbations whose spread varies by view (the "epistemic" signal), and
+# per-channel posterior variances.  No method arithmetic here.
+# --------------------------------------------------------------------------
+def gen_latent_ensembles(n_views: int = 1000, M: int = 5, C: int = 4, H: int = 64, W: int = 64, seed: int = 0):
+    """-> (mu, s2) float32 arrays [n_views][M][C][H*W]."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    spread = rng.uniform(0.05, 0.5, size=(n_views, 1, 1, 1))
+    base = rng.normal(0.0, 1.0, size=(n_views, 1, C, H * W))
+    mu = base + spread * rng.normal(0.0, 1.0, size=(n_views, M, C, H * W))
+    s2 = np.exp(rng.normal(-2.0, 0.3, size=(n_views, M, C, H * W)))
+    return np.ascontiguousarray(mu, dtype=np.float32), np.ascontiguousarray(s2, dtype=np.float32)
