@@ -105,16 +105,28 @@ gsr_status gsr_camera_look_at(double elevation, double azimuth, double radius, c
 /* ---- K1: projection + culling (north_star "projection/culling kernel") ----
    For every (view c, Gaussian g) of the batch: view transform, near cull
    (vz > znear), EWA 2D covariance with 0.3 px^2 dilation and 1.3x FOV clamp,
-   det cull, conic, radius r = ceil(3.33 sqrt(lambda_max)), 16x16 tile rect,
-   SH colour (degree <= 3), depth-key bits (O1/O4).
-   cams        [host] n_views cameras, all with the same W,H (n_views <= GSR_MAX_VIEWS)
+   det cull, conic, tile spans, SH colour (degree <= 3), depth-key bits
+   (O1/O4).  Tile spans (O1 steps 14-15): with Sigma' = [[a,b],[b,c]]
+   and t = 11.1 (> 3.33^2 > 2 ln 255), m = 1/16 px, the pixel rows
+   py0..py1 are those whose centre lies within v -/+ (sqrt(t c) + m); for each
+   tile row ty the band of its pixel rows [ya, yb] gives
+     R = ((u + p dr) + sqrt(max(0, h (t - dr^2 / c)))) + m,  dr = clamp(dys, ya+.5-v, yb+.5-v)
+     L = ((u + p dl) - sqrt(max(0, h (t - dl^2 / c)))) - m,  dl = clamp(-dys, ...)
+   (p = b/c, h = det/c, dys = b sqrt(t/a): the ellipse's x-interval over the
+   band), and the span is the tiles holding a pixel column centre in [L, R]
+   clipped to the image.  n_tiles = sum of span widths (0 = culled).
+   cams        [host] n_views cameras, all with the same W,H (n_views <= GSR_MAX_VIEWS;
+               W, H <= 65535)
    render_rec  [V][n][12] float: (u, v, A, B), (C, opacity, uncertainty, tau),
                (r, g, b, ext) -- conic (A,B,C) = inverse 2D covariance; tau =
                -ln(255 opacity) - 1e-3 (alpha-skip pre-test bound); ext = two
                round-up fp16 half-extents of the alpha >= 1/255 ellipse.  Written
                only where n_tiles > 0 (culled records are left untouched).
-   bin_rec     [4][V][n] uint32 planes: depth bits of view-space z, x0 | x1 << 16,
-               y0 | y1 << 16, n_tiles (0 = culled; then the other planes are 0). */
+   bin_rec     uint32 [10 V n], 16-byte aligned:
+               words [0, 8Vn): span records [V][n][8] = (u, v, p, h, 1/c, dys,
+                               py0 | py1 << 16, n_tiles), written only where n_tiles > 0;
+               words [8Vn, 9Vn): depth bits of view-space z [V][n] (0 when culled);
+               words [9Vn, 10Vn): n_tiles [V][n] (0 = culled). */
 gsr_status gsr_project(gsr_ctx* ctx, const gsr_gaussians* gaussians, const gsr_camera* cams,
                        int32_t n_views, float* render_rec, uint32_t* bin_rec, void* stream);
 
@@ -122,7 +134,7 @@ gsr_status gsr_project(gsr_ctx* ctx, const gsr_gaussians* gaussians, const gsr_c
    Produces the (view, tile)-sorted Gaussian lists of the batch.  Key of a
    duplicated entry = ((view_in_batch * gx*gy + ty*gx + tx) << 32) | depth bits,
    value = g; the sorted order is (key, value) lexicographic (O2/O3).
-   bin_rec     [4][V][n] from gsr_project; n = Gaussians per view
+   bin_rec     [10 V n] from gsr_project (same n_views); n = Gaussians per view
    cams        [host] the batch's cameras (same W,H)
    keys        [capacity] uint64, OPTIONAL (NULL: the sorted 64-bit keys are not
                materialised -- the composite needs only vals + ranges)
@@ -132,7 +144,8 @@ gsr_status gsr_project(gsr_ctx* ctx, const gsr_gaussians* gaussians, const gsr_c
                waits for the count (one 8-byte readback per batch)
    ranges      [V*gx*gy][2] uint32 [start, end) per (view, tile); empty = [s, s)
    keys_unsorted / vals_unsorted  OPTIONAL [capacity]: the duplicated list in
-               emission order (view, g ascending, ty, tx) -- for parity tests
+               emission order (view, g ascending, ty ascending, tx ascending over
+               each row's span) -- for parity tests
    Returns GSR_ECAPACITY (with *n_keys = K, nothing else written) if K > capacity. */
 gsr_status gsr_bin_sort(gsr_ctx* ctx, const uint32_t* bin_rec, int64_t n, const gsr_camera* cams,
                         int32_t n_views, uint64_t* keys, uint32_t* vals, int64_t capacity,

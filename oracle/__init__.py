@@ -32,9 +32,10 @@ CFLAGS = ["-O2", "-std=c11", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-s
 
 PROJ_DTYPE = np.dtype(
     [("u", "<f4"), ("v", "<f4"), ("A", "<f4"), ("B", "<f4"), ("C", "<f4"), ("o", "<f4"),
-     ("unc", "<f4"), ("r", "<f4"), ("g", "<f4"), ("b", "<f4"), ("depth_bits", "<u4"),
-     ("x0", "<u4"), ("x1", "<u4"), ("y0", "<u4"), ("y1", "<u4"), ("n_tiles", "<u4")])
-assert PROJ_DTYPE.itemsize == 64
+     ("unc", "<f4"), ("r", "<f4"), ("g", "<f4"), ("b", "<f4"),
+     ("sp_p", "<f4"), ("sp_h", "<f4"), ("sp_ic", "<f4"), ("sp_dys", "<f4"),
+     ("depth_bits", "<u4"), ("py0", "<u4"), ("py1", "<u4"), ("n_tiles", "<u4")])
+assert PROJ_DTYPE.itemsize == 72
 
 TILE = 16
 
@@ -61,6 +62,7 @@ def lib():
         L.orc_exp_spec.restype = ctypes.c_float
         L.orc_sh_basis.argtypes = [ctypes.c_float] * 3 + [P]
         L.orc_project.argtypes = [P, i64, ctypes.c_int, P, P]
+        L.orc_row_span.argtypes = [P, ctypes.c_uint32, ctypes.c_int, P, P]
         L.orc_count_keys.argtypes = [P, i64]
         L.orc_count_keys.restype = i64
         L.orc_emit_keys.argtypes = [P, i64, P, i32, P, P]
@@ -117,6 +119,27 @@ def project(field, cam) -> np.ndarray:
     c = _cam(cam)
     out = np.zeros(field.n, dtype=PROJ_DTYPE)
     L.orc_project(_p(planes), field.n, field.sh_degree, _p(c), _p(out))
+    return out
+
+
+def row_span(proj_one, ty: int, cam):
+    """O1 step 15: tile-column span [x0, x1) of tile row ``ty`` of one
+    projected Gaussian (x0 = x1 = 0 when empty)."""
+    L = lib()
+    p = np.ascontiguousarray(np.asarray(proj_one, dtype=PROJ_DTYPE).reshape(1))
+    x0, x1 = ctypes.c_uint32(0), ctypes.c_uint32(0)
+    L.orc_row_span(_p(p), int(ty), _wh(cam)[0], ctypes.byref(x0), ctypes.byref(x1))
+    return int(x0.value), int(x1.value)
+
+
+def tiles_of(proj_one, cam):
+    """All (ty, tx) tiles of one projected Gaussian in emission order."""
+    if int(proj_one["n_tiles"]) == 0:
+        return []
+    out = []
+    for ty in range(int(proj_one["py0"]) >> 4, (int(proj_one["py1"]) >> 4) + 1):
+        x0, x1 = row_span(proj_one, ty, cam)
+        out.extend((ty, tx) for tx in range(x0, x1))
     return out
 
 

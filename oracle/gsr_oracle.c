@@ -41,12 +41,20 @@ typedef struct {
 /* one projected (view, Gaussian) pair */
 typedef struct {
   float u, v, A, B, C, o, unc, r, g, b;
-  uint32_t depth_bits, x0, x1, y0, y1, n_tiles;
+  /* tile-span parameters (O1 step 15): x-shift per row p = b/c,
+     conditional x-variance h = det/c, 1/c, and dy of the rightmost point */
+  float sp_p, sp_h, sp_ic, sp_dys;
+  uint32_t depth_bits, py0, py1, n_tiles; /* py0..py1: pixel rows of the span extent */
 } orc_proj;
 
 /* SURVEY.md Appendix A, retyped as literals */
 static const float ORC_DILATION = 0.3f;
-static const float ORC_RADIUS_K = 3.33f;
+/* span ellipse q <= ORC_SPAN_T and margin (O1 step 14): 11.1 > 3.33^2 =
+   11.0889 > 2 ln 255 = 11.0825, so every pixel with alpha >= 1/255 lies inside
+   q <= 11.0889; the 1e-3 relative inflation and the 1/16 px margin absorb the
+   float32 rounding of the span arithmetic. */
+static const float ORC_SPAN_T = 11.1f;
+static const float ORC_SPAN_M = 0.0625f;
 static const float ORC_ALPHA_MIN = 1.0f / 255.0f;  /* 0x3b808081 */
 static const float ORC_ALPHA_MAX = 0.99f;
 static const float ORC_T_STOP = 1e-4f;
@@ -111,7 +119,29 @@ void orc_sh_basis(float x, float y, float z, float Y[16]) {
   Y[15] = (-SH_C3a * x) * (xx - (3.0f * yy));
 }
 
-static float clampf_(float v, float lo, float hi) { return v < lo ? lo : (v > hi ? hi : v); }
+/* O1 step 15: span [x0, x1) of tile columns of tile row ty.  The pixel rows
+   of the tile inside [py0, py1] form the band [ya, yb]; over the band the
+   ellipse q <= t, whose x-interval at offset dy is
+     p dy -/+ sqrt(h (t - dy^2 / c)),
+   reaches furthest right at dy = dys (its rightmost point) and furthest left
+   at dy = -dys, so both bounds are taken at those offsets clamped into the
+   band.  Columns with a pixel centre in [L, R] (widened by m), clipped to the
+   image, give the tile columns.  Empty spans give x0 = x1 = 0. */
+void orc_row_span(const orc_proj* p, uint32_t ty, int W, uint32_t* x0, uint32_t* x1) {
+  uint32_t ya = ty * 16u > p->py0 ? ty * 16u : p->py0;
+  uint32_t yb = ty * 16u + 15u < p->py1 ? ty * 16u + 15u : p->py1;
+  float dya = ((float)ya + 0.5f) - p->v;
+  float dyb = ((float)yb + 0.5f) - p->v;
+  float dr = fminf(fmaxf(p->sp_dys, dya), dyb);
+  float dl = fminf(fmaxf(-p->sp_dys, dya), dyb);
+  float R = ((p->u + p->sp_p * dr) + sqrtf(fmaxf(0.0f, p->sp_h * (ORC_SPAN_T - (dr * dr) * p->sp_ic)))) + ORC_SPAN_M;
+  float L = ((p->u + p->sp_p * dl) - sqrtf(fmaxf(0.0f, p->sp_h * (ORC_SPAN_T - (dl * dl) * p->sp_ic)))) - ORC_SPAN_M;
+  float fpx0 = fmaxf(ceilf(L - 0.5f), 0.0f);
+  float fpx1 = fminf(floorf(R - 0.5f), (float)(W - 1));
+  if (!(fpx0 <= fpx1)) { *x0 = 0; *x1 = 0; return; }
+  *x0 = (uint32_t)fpx0 >> 4;
+  *x1 = ((uint32_t)fpx1 >> 4) + 1u;
+}
 
 /* planes: float32 [P][n][4]; plane 0 (x,y,z,o), 1 (sx,sy,sz,unc), 2 (qw,qx,qy,qz),
    3.. SH slot-major.  Projects Gaussian g into camera cam. */
@@ -180,32 +210,39 @@ void orc_project_one(const float* planes, int64_t n, int sh_degree, const orc_ca
   /* 13. determinant cull */
   float det = a * c - b * b;
   if (!(det > 0.0f)) return;
-  /* 14. radius */
-  float mid = 0.5f * (a + c);
-  float lam = mid + sqrtf(fmaxf(mid * mid - det, 0.0f));
-  float r = ceilf(ORC_RADIUS_K * sqrtf(lam));
-  /* 15. tile rect */
-  int gx = (cam->width + ORC_TILE - 1) / ORC_TILE;
-  int gy = (cam->height + ORC_TILE - 1) / ORC_TILE;
-  float fx0 = clampf_(floorf((u - r) * 0.0625f), 0.0f, (float)gx);
-  float fx1 = clampf_(ceilf((u + r) * 0.0625f), 0.0f, (float)gx);
-  float fy0 = clampf_(floorf((v - r) * 0.0625f), 0.0f, (float)gy);
-  float fy1 = clampf_(ceilf((v + r) * 0.0625f), 0.0f, (float)gy);
-  uint32_t x0 = (uint32_t)fx0, x1 = (uint32_t)fx1, y0 = (uint32_t)fy0, y1 = (uint32_t)fy1;
-  uint32_t nt = (x1 - x0) * (y1 - y0);
-  if (nt == 0) return;
+  /* 14. span extent: pixel rows whose centre lies within the y-extent of the
+     ellipse q <= t (t = ORC_SPAN_T), widened by the margin m */
+  const int W = cam->width, H = cam->height;
+  float ye = sqrtf(ORC_SPAN_T * c) + ORC_SPAN_M;
+  float fpy0 = fmaxf(ceilf((v - ye) - 0.5f), 0.0f);
+  float fpy1 = fminf(floorf((v + ye) - 0.5f), (float)(H - 1));
+  if (!(fpy0 <= fpy1)) return;
+  out->u = u;
+  out->v = v;
+  out->sp_p = b / c;
+  out->sp_h = det / c;
+  out->sp_ic = 1.0f / c;
+  out->sp_dys = b * sqrtf(ORC_SPAN_T / a);
+  out->py0 = (uint32_t)fpy0;
+  out->py1 = (uint32_t)fpy1;
+  /* 15. tile spans: n_tiles = sum over tile rows of the row's span width */
+  uint32_t nt = 0;
+  for (uint32_t ty = out->py0 >> 4; ty <= (out->py1 >> 4); ++ty) {
+    uint32_t x0, x1;
+    orc_row_span(out, ty, W, &x0, &x1);
+    nt += x1 - x0;
+  }
+  if (nt == 0) { memset(out, 0, sizeof(*out)); return; }
   /* 16. conic */
   float inv = 1.0f / det;
   out->A = c * inv;
   out->B = -(b * inv);
   out->C = a * inv;
-  out->u = u;
-  out->v = v;
   out->o = o;
   out->unc = su[3];
   /* 17. depth key */
   out->depth_bits = f2u(vz);
-  out->x0 = x0; out->x1 = x1; out->y0 = y0; out->y1 = y1; out->n_tiles = nt;
+  out->n_tiles = nt;
   /* O4: SH colour */
   float dx = mx - cam->campos[0], dy = my - cam->campos[1], dz = mz - cam->campos[2];
   float len = sqrtf((dx * dx + dy * dy) + dz * dz);
@@ -244,13 +281,16 @@ void orc_emit_keys(const orc_proj* p, int64_t n, const orc_camera* cam, int32_t 
   int64_t k = 0;
   for (int64_t g = 0; g < n; ++g) {
     if (p[g].n_tiles == 0) continue;
-    for (uint32_t ty = p[g].y0; ty < p[g].y1; ++ty)
-      for (uint32_t tx = p[g].x0; tx < p[g].x1; ++tx) {
+    for (uint32_t ty = p[g].py0 >> 4; ty <= (p[g].py1 >> 4); ++ty) {
+      uint32_t x0, x1;
+      orc_row_span(&p[g], ty, cam->width, &x0, &x1);
+      for (uint32_t tx = x0; tx < x1; ++tx) {
         uint64_t tile = (uint64_t)view_in_batch * gx * gy + (uint64_t)ty * gx + tx;
         keys[k] = (tile << 32) | (uint64_t)p[g].depth_bits;
         vals[k] = (uint32_t)g;
         ++k;
       }
+    }
   }
 }
 

@@ -205,16 +205,17 @@ gsr_status gsr_project(gsr_ctx* ctx, const gsr_gaussians* G, const gsr_camera* c
   }
   const uint64_t tiles = (uint64_t)((W + kTile - 1) / kTile) * (uint64_t)((H + kTile - 1) / kTile);
   if (tiles * (uint64_t)n_views >= (1ull << 32)) return set_err(ctx, GSR_EINVAL, "gsr_project: V*tiles >= 2^32");
-  if (((W + kTile - 1) / kTile) >= 65536 || ((H + kTile - 1) / kTile) >= 65536)
-    return set_err(ctx, GSR_EINVAL, "gsr_project: tile grid too wide for 16-bit rect fields");
+  if (W > 65535 || H > 65535)
+    return set_err(ctx, GSR_EINVAL, "gsr_project: W or H > 65535 (16-bit pixel-row fields of the span record)");
   if (G->n == 0) return GSR_OK;
   CamBatch cb;
   std::memset(&cb, 0, sizeof(cb));
   std::memcpy(cb.c, cams, sizeof(gsr_camera) * (size_t)n_views);
-  // algorithmic bytes: parameter planes once per batch + bin planes; the 48-byte
-  // render records of the visible pairs are added by gsr_bin_sort (it knows N_vis)
+  // algorithmic bytes: parameter planes once per batch + depth / n_tiles planes; the
+  // 48-byte render records and 32-byte span records of the visible pairs are added
+  // by gsr_bin_sort (it knows N_vis)
   const int planes = 3 + (3 * (G->sh_degree + 1) * (G->sh_degree + 1) + 3) / 4;
-  account(ctx, GSR_STAGE_PROJECT, 1, 16.0 * planes * (double)G->n + 16.0 * n_views * (double)G->n);
+  account(ctx, GSR_STAGE_PROJECT, 1, 16.0 * planes * (double)G->n + 8.0 * n_views * (double)G->n);
   StageScope sc(ctx, GSR_STAGE_PROJECT, (cudaStream_t)stream);
   return check_cuda(ctx, launch_project(*G, cb, n_views, render_rec, bin_rec, (cudaStream_t)stream), "k1_project");
 }

@@ -752,24 +752,37 @@ cudaError_t launch_pass(const KeyT* kin, const uint32_t* vin, KeyT* kout, uint32
 
 // ---------------------------------------------------------------------------
 // K3: look-back scan of n_tiles in depth-sorted order + load-balanced emission.
-// Block = 8 warps x 8 rounds x 32 entries = 2048 entries; warp w owns 256
-// consecutive entries.
-constexpr int K3_ROUNDS = 8;
+// Block = 8 warps x K3_ROUNDS rounds x 32 entries; warp w owns 32 * K3_ROUNDS
+// consecutive entries.  Each entry's 32-byte span record (O1 step
+// 15) is gathered once.  Emission is two-level load-balanced: the warp's
+// (entry, tile row) units are dealt 32 at a time (owner search over the row
+// counts), each lane evaluates its unit's span, and the keys of the 32 spans
+// are dealt 32 at a time (owner search over the span widths).  Keys leave in
+// unit order, i.e. (depth, g, ty, tx) order, contiguously from the block's
+// look-back offset.
+constexpr int K3_ROUNDS = 4;
 constexpr int K3_TILE = 256 * K3_ROUNDS;
 
+__device__ __forceinline__ int owner_of(uint32_t excl, uint32_t j) {  // largest s with excl[s] <= j
+  int s = 0;
+#pragma unroll
+  for (int step = 16; step > 0; step >>= 1) {
+    const uint32_t e = __shfl_sync(FULL, excl, s + step);
+    if (e <= j) s += step;
+  }
+  return s;
+}
+
 __global__ void __launch_bounds__(256) k3_emit(const uint64_t* __restrict__ dkeys, const uint32_t* __restrict__ dvals,
-                                               int64_t nvis, const uint32_t* __restrict__ xr_plane,
-                                               const uint32_t* __restrict__ yr_plane,
-                                               const uint32_t* __restrict__ nt_plane, int64_t n, uint32_t gx,
-                                               uint32_t tpv, uint32_t* __restrict__ tkeys,
+                                               int64_t nvis, const uint4* __restrict__ span, int64_t n, uint32_t gx,
+                                               uint32_t tpv, int W, uint32_t* __restrict__ tkeys,
                                                uint32_t* __restrict__ tvals, uint32_t* __restrict__ counts,
                                                uint64_t* __restrict__ lb, uint32_t* __restrict__ ctr,
                                                int smem_bins) {
-  // Per-tile counts: warp-aggregated (match_any + one atomic per distinct tile
-  // in the warp) into a shared-memory histogram over the tiles of the block's
+  // Per-tile counts: a shared-memory histogram over the tiles of the block's
   // first view (a depth-sorted block almost always lies in one view), flushed
   // with one global atomic per non-empty bin; other views go straight to
-  // global memory (still warp-aggregated).
+  // global memory.
   extern __shared__ uint32_t s_cnt[];
   __shared__ uint64_t s_w[8];
   __shared__ uint64_t s_prefix;
@@ -786,22 +799,25 @@ __global__ void __launch_bounds__(256) k3_emit(const uint64_t* __restrict__ dkey
   const uint32_t view0 = s_view0;
   const uint32_t lo = view0 * tpv;
   const int64_t e0 = bid * K3_TILE + (int64_t)warp * (32 * K3_ROUNDS);
-  uint32_t nt[K3_ROUNDS], xr[K3_ROUNDS], yr[K3_ROUNDS], g[K3_ROUNDS], view[K3_ROUNDS];
+  uint4 s0[K3_ROUNDS], s1[K3_ROUNDS];
+  uint32_t g[K3_ROUNDS], view[K3_ROUNDS];
   uint64_t mine = 0;
 #pragma unroll
   for (int r = 0; r < K3_ROUNDS; ++r) {
     const int64_t e = e0 + r * 32 + lane;
-    nt[r] = 0; xr[r] = 0; yr[r] = 0; g[r] = 0; view[r] = 0;
+    s0[r] = make_uint4(0, 0, 0, 0);
+    s1[r] = make_uint4(0, 0, 0, 0);
+    g[r] = 0;
+    view[r] = 0;
     if (e < nvis) {
       const uint64_t key = dkeys[e];
       g[r] = dvals[e];
       view[r] = (uint32_t)(key >> 32);
       const int64_t pi = (int64_t)view[r] * n + g[r];
-      nt[r] = __ldg(nt_plane + pi);
-      xr[r] = __ldg(xr_plane + pi);
-      yr[r] = __ldg(yr_plane + pi);
+      s0[r] = __ldg(span + 2 * pi);
+      s1[r] = __ldg(span + 2 * pi + 1);
     }
-    mine += nt[r];
+    mine += s1[r].w;
   }
   const uint64_t wtot = warp_sum<uint64_t>(mine);
   if (lane == 0) s_w[warp] = wtot;
@@ -825,51 +841,54 @@ __global__ void __launch_bounds__(256) k3_emit(const uint64_t* __restrict__ dkey
   uint64_t base = s_prefix + s_w[warp];
 #pragma unroll
   for (int r = 0; r < K3_ROUNDS; ++r) {
-    const uint32_t inc = warp_incl_scan<uint32_t>(nt[r]);
-    const uint32_t excl = inc - nt[r];
-    const uint32_t total = __shfl_sync(FULL, inc, 31);
-    // per entry: key of the rect's first tile, rect width and its reciprocal
-    const uint32_t x0 = xr[r] & 0xffffu, wdt = max((xr[r] >> 16) - x0, 1u), y0 = yr[r] & 0xffffu;
-    const uint32_t kbase = view[r] * tpv + y0 * gx + x0;
-    const float rcp = __frcp_rn((float)wdt);
-    for (uint32_t jb = 0; jb < total; jb += 32) {
-      const uint32_t j = jb + lane;
-      // owner lane: largest s with excl[s] <= j
-      int s = 0;
-#pragma unroll
-      for (int step = 16; step > 0; step >>= 1) {
-        const uint32_t e = __shfl_sync(FULL, excl, s + step);
-        if (e <= j) s += step;
-      }
-      const uint32_t oexcl = __shfl_sync(FULL, excl, s);
-      const uint32_t okb = __shfl_sync(FULL, kbase, s), ow = __shfl_sync(FULL, wdt, s);
-      const float orcp = __shfl_sync(FULL, rcp, s);
+    const uint32_t pyr = s1[r].z;
+    const uint32_t nrows = s1[r].w ? (pyr >> 20) - ((pyr & 0xffffu) >> 4) + 1u : 0u;
+    const uint32_t rinc = warp_incl_scan<uint32_t>(nrows);
+    const uint32_t rexcl = rinc - nrows;
+    const uint32_t rtot = __shfl_sync(FULL, rinc, 31);
+    for (uint32_t ub = 0; ub < rtot; ub += 32) {
+      const uint32_t j = ub + lane;
+      const int s = owner_of(rexcl, j);
+      const float u = __uint_as_float(__shfl_sync(FULL, s0[r].x, s));
+      const float v = __uint_as_float(__shfl_sync(FULL, s0[r].y, s));
+      const float sp = __uint_as_float(__shfl_sync(FULL, s0[r].z, s));
+      const float sh = __uint_as_float(__shfl_sync(FULL, s0[r].w, s));
+      const float sic = __uint_as_float(__shfl_sync(FULL, s1[r].x, s));
+      const float sdys = __uint_as_float(__shfl_sync(FULL, s1[r].y, s));
+      const uint32_t opyr = __shfl_sync(FULL, pyr, s);
+      const uint32_t oex = __shfl_sync(FULL, rexcl, s);
       const uint32_t og = __shfl_sync(FULL, g[r], s);
-      if (j < total) {
-        const uint32_t loc = j - oexcl;
-        uint32_t q = __float2uint_rz((float)loc * orcp);  // loc < 2^24: off by at most one
-        uint32_t rem = loc - q * ow;
-        if ((int32_t)rem < 0) {
-          --q;
-          rem += ow;
-        } else if (rem >= ow) {
-          ++q;
-          rem -= ow;
-        }
-        const uint32_t key = okb + q * gx + rem;
-        tkeys[base + j] = key;
-        tvals[base + j] = og;
-        // Tile counts: shared-memory histogram of the block's view (aggregated
-        // per block, flushed with one global atomic per non-empty bin).  A
-        // MATCH.ANY warp aggregation was measured to cost more than it saved:
-        // keys of one 32-key window are almost always distinct tiles.
-        if (key - lo < (uint32_t)smem_bins)
-          atomicAdd(s_cnt + (key - lo), 1u);
-        else
-          atomicAdd(counts + key, 1u);
+      const uint32_t ov = __shfl_sync(FULL, view[r], s);
+      uint32_t w = 0, kb = 0;
+      if (j < rtot) {
+        const uint32_t py0 = opyr & 0xffffu, py1 = opyr >> 16;
+        const uint32_t ty = (py0 >> 4) + (j - oex);
+        uint32_t x0, x1;
+        row_span(u, v, sp, sh, sic, sdys, py0, py1, ty, W, x0, x1);
+        w = x1 - x0;
+        kb = ov * tpv + ty * gx + x0;
       }
+      const uint32_t winc = warp_incl_scan<uint32_t>(w);
+      const uint32_t wexcl = winc - w;
+      const uint32_t wt = __shfl_sync(FULL, winc, 31);
+      for (uint32_t kb0 = 0; kb0 < wt; kb0 += 32) {
+        const uint32_t k = kb0 + lane;
+        const int t = owner_of(wexcl, k);
+        const uint32_t okb = __shfl_sync(FULL, kb, t);
+        const uint32_t owx = __shfl_sync(FULL, wexcl, t);
+        const uint32_t ogg = __shfl_sync(FULL, og, t);
+        if (k < wt) {
+          const uint32_t key = okb + (k - owx);
+          tkeys[base + k] = key;
+          tvals[base + k] = ogg;
+          if (key - lo < (uint32_t)smem_bins)
+            atomicAdd(s_cnt + (key - lo), 1u);
+          else
+            atomicAdd(counts + key, 1u);
+        }
+      }
+      base += wt;
     }
-    base += total;
   }
   __syncthreads();
   for (int t = tid; t < smem_bins; t += 256) {
@@ -946,11 +965,10 @@ __global__ void __launch_bounds__(1024) k5_ranges(const uint32_t* __restrict__ c
 
 // O2 emission order (view, g, ty, tx): parity output only.
 __global__ void __launch_bounds__(256) k_emit_o2(const uint32_t* __restrict__ depth_plane,
-                                                 const uint32_t* __restrict__ xr_plane,
-                                                 const uint32_t* __restrict__ yr_plane,
+                                                 const uint4* __restrict__ span,
                                                  const uint32_t* __restrict__ nt_plane,
                                                  const uint32_t* __restrict__ emit_off, int64_t M, int64_t n,
-                                                 uint32_t gx, uint32_t tpv, uint64_t* __restrict__ keys,
+                                                 uint32_t gx, uint32_t tpv, int W, uint64_t* __restrict__ keys,
                                                  uint32_t* __restrict__ vals) {
   const int64_t i = (int64_t)blockIdx.x * 256 + threadIdx.x;
   if (i >= M) return;
@@ -958,15 +976,21 @@ __global__ void __launch_bounds__(256) k_emit_o2(const uint32_t* __restrict__ de
   if (!nt) return;
   const uint64_t view = (uint64_t)(i / n);
   const uint32_t g = (uint32_t)(i - (int64_t)view * n);
-  const uint32_t xr = xr_plane[i], yr = yr_plane[i], d = depth_plane[i];
+  const uint4 a = span[2 * i], b = span[2 * i + 1];
+  const uint32_t d = depth_plane[i];
+  const uint32_t py0 = b.z & 0xffffu, py1 = b.z >> 16;
   uint64_t o = emit_off[i];
-  for (uint32_t ty = yr & 0xffffu; ty < (yr >> 16); ++ty)
-    for (uint32_t tx = xr & 0xffffu; tx < (xr >> 16); ++tx) {
+  for (uint32_t ty = py0 >> 4; ty <= (py1 >> 4); ++ty) {
+    uint32_t x0, x1;
+    row_span(__uint_as_float(a.x), __uint_as_float(a.y), __uint_as_float(a.z), __uint_as_float(a.w),
+             __uint_as_float(b.x), __uint_as_float(b.y), py0, py1, ty, W, x0, x1);
+    for (uint32_t tx = x0; tx < x1; ++tx) {
       const uint64_t tile = view * tpv + (uint64_t)ty * gx + tx;
       keys[o] = (tile << 32) | d;
       vals[o] = g;
       ++o;
     }
+  }
 }
 
 int bits_for(uint64_t count) {  // ceil(log2(count)), 0 for count <= 1
@@ -1132,10 +1156,9 @@ extern "C" gsr_status gsr_bin_sort(gsr_ctx* ctx, const uint32_t* bin_rec, int64_
   cudaStream_t st = (cudaStream_t)stream;
   gsr_status s;
 
-  const uint32_t* p_depth = bin_rec;
-  const uint32_t* p_xr = bin_rec + M;
-  const uint32_t* p_yr = bin_rec + 2 * M;
-  const uint32_t* p_nt = bin_rec + 3 * M;
+  const uint4* p_span = reinterpret_cast<const uint4*>(bin_rec);  // [M][2] span records
+  const uint32_t* p_depth = bin_rec + 8 * M;
+  const uint32_t* p_nt = bin_rec + 9 * M;
 
   const int vbits = bits_for((uint64_t)n_views);
   const int dpasses = (32 + vbits + 7) / 8;               // depth sort passes
@@ -1185,7 +1208,7 @@ extern "C" gsr_status gsr_bin_sort(gsr_ctx* ctx, const uint32_t* bin_rec, int64_
   // the visible ones, writes 12 B per visible pair; K1's 48-B render records of
   // the visible pairs are attributed to the projection stage.
   account(ctx, GSR_STAGE_COMPACT, M > 0 ? 1 : 0, 4.0 * M + 16.0 * nvis);
-  account(ctx, GSR_STAGE_PROJECT, 0, 48.0 * nvis);
+  account(ctx, GSR_STAGE_PROJECT, 0, 80.0 * nvis);
   if (K > capacity) return set_err(ctx, GSR_ECAPACITY, "gsr_bin_sort: capacity too small (n_keys = required)");
   if (K >= (1ll << 31)) return set_err(ctx, GSR_EINVAL, "gsr_bin_sort: K >= 2^31 keys in one batch");
 
@@ -1245,11 +1268,10 @@ extern "C" gsr_status gsr_bin_sort(gsr_ctx* ctx, const uint32_t* bin_rec, int64_
   // ---- K3: emission + counts ----
   sp = stage_begin(ctx, GSR_STAGE_EMIT, st);
   const int bins = tpv <= 12288 ? (int)tpv : 0;  // <= 48 KB of shared memory
-  k3_emit<<<(unsigned)nb3, 256, bins * 4, st>>>(ck, cvv, nvis, p_xr, p_yr, p_nt, n, gx, (uint32_t)tpv,
-                                                (uint32_t*)tka, (uint32_t*)tva, (uint32_t*)cnt, lb3, ctrs + 5,
-                                                bins);
+  k3_emit<<<(unsigned)nb3, 256, bins * 4, st>>>(ck, cvv, nvis, p_span, n, gx, (uint32_t)tpv, W, (uint32_t*)tka,
+                                                (uint32_t*)tva, (uint32_t*)cnt, lb3, ctrs + 5, bins);
   stage_end(ctx, sp, st);
-  account(ctx, GSR_STAGE_EMIT, 1, 24.0 * nvis + 8.0 * K + 4.0 * T);
+  account(ctx, GSR_STAGE_EMIT, 1, 44.0 * nvis + 8.0 * K + 4.0 * T);
   if ((s = check_cuda(ctx, cudaGetLastError(), "k3_emit")) != GSR_OK) return s;
 
   // ---- K5: ranges + tile-sort histograms ----
@@ -1291,8 +1313,8 @@ extern "C" gsr_status gsr_bin_sort(gsr_ctx* ctx, const uint32_t* bin_rec, int64_
   // ---- optional O2 emission-order list ----
   if (keys_unsorted) {
     account(ctx, GSR_STAGE_EMIT, 1, 16.0 * M + 12.0 * K);
-    k_emit_o2<<<(unsigned)((M + 255) / 256), 256, 0, st>>>(p_depth, p_xr, p_yr, p_nt, (const uint32_t*)eo, M, n, gx,
-                                                           (uint32_t)tpv, keys_unsorted, vals_unsorted);
+    k_emit_o2<<<(unsigned)((M + 255) / 256), 256, 0, st>>>(p_depth, p_span, p_nt, (const uint32_t*)eo, M, n, gx,
+                                                           (uint32_t)tpv, W, keys_unsorted, vals_unsorted);
     if ((s = check_cuda(ctx, cudaGetLastError(), "emit_o2")) != GSR_OK) return s;
   }
   return GSR_OK;

@@ -47,6 +47,36 @@ __device__ __forceinline__ float exp_spec_core(float x) {  // x in [-80, 0]
 }
 __device__ __forceinline__ float exp_spec(float x) { return x < -80.0f ? 0.0f : exp_spec_core(x); }
 
+// ---- tile spans (O1 steps 14-15) ----
+// A Gaussian is listed in tile (tx, ty) iff the tile holds a pixel centre
+// inside the x-extent, over the tile's pixel rows, of the ellipse q <= 11.1
+// (> 3.33^2 > 2 ln 255: contains every alpha >= 1/255 pixel) widened by
+// 1/16 px.  K1 stores the span parameters once per visible (view, g) in a
+// 32-byte record; K1 (counting) and K3 (emitting) evaluate the same span
+// function on the same floats, so n_tiles and the emitted keys agree exactly.
+constexpr float kSpanT = 11.1f;      // 0x4131999a
+constexpr float kSpanM = 0.0625f;    // 1/16 px
+// span record [V*n][2] uint4: (u, v, p = b/c, h = det/c), (1/c, dys, py0 | py1 << 16, n_tiles)
+__device__ __forceinline__ void row_span(float u, float v, float p, float h, float ic, float dys, uint32_t py0,
+                                         uint32_t py1, uint32_t ty, int W, uint32_t& x0, uint32_t& x1) {
+  const uint32_t ya = max(ty * 16u, py0), yb = min(ty * 16u + 15u, py1);
+  const float dya = ((float)ya + 0.5f) - v;
+  const float dyb = ((float)yb + 0.5f) - v;
+  const float dr = fminf(fmaxf(dys, dya), dyb);
+  const float dl = fminf(fmaxf(-dys, dya), dyb);
+  const float R = ((u + p * dr) + sqrtf(fmaxf(0.0f, h * (kSpanT - (dr * dr) * ic)))) + kSpanM;
+  const float L = ((u + p * dl) - sqrtf(fmaxf(0.0f, h * (kSpanT - (dl * dl) * ic)))) - kSpanM;
+  const float fx0 = fmaxf(ceilf(L - 0.5f), 0.0f);
+  const float fx1 = fminf(floorf(R - 0.5f), (float)(W - 1));
+  if (fx0 <= fx1) {
+    x0 = (uint32_t)fx0 >> 4;
+    x1 = ((uint32_t)fx1 >> 4) + 1u;
+  } else {
+    x0 = 0u;
+    x1 = 0u;
+  }
+}
+
 // ---- context scratch ----
 enum Slot {
   S_DKEY_A, S_DKEY_B, S_DVAL_A, S_DVAL_B,   // depth pre-sort (visible (view,g) pairs)

@@ -74,7 +74,7 @@ __device__ __forceinline__ float clampf(float v, float lo, float hi) { return fm
 template <int DEG>
 __global__ void __launch_bounds__(256) k1_project(const float4* __restrict__ po, const float4* __restrict__ su,
                                                   const float4* __restrict__ rq, const float4* __restrict__ sh,
-                                                  int64_t n, int V, int gx, int gy,
+                                                  int64_t n, int V, int W, int H,
                                                   const __grid_constant__ CamBatch cams,
                                                   float4* __restrict__ rec, uint32_t* __restrict__ bin) {
   const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -121,11 +121,14 @@ __global__ void __launch_bounds__(256) k1_project(const float4* __restrict__ po,
   const float thr = 2.0f * logf(255.0f * o) + 2e-3f;  // q threshold of the alpha >= 1/255 region
 
   const int64_t VN = (int64_t)V * n;
+  uint4* span = reinterpret_cast<uint4*>(bin);        // [V*n][2] span records
+  uint32_t* depth_plane = bin + 8 * VN;               // [V*n]
+  uint32_t* nt_plane = bin + 9 * VN;                  // [V*n]
   for (int c = 0; c < V; ++c) {
     const gsr_camera& cam = cams.c[c];
     const float* R = cam.R;
     const int64_t cg = (int64_t)c * n + g;
-    uint32_t depth = 0, xr = 0, yr = 0, nt = 0;
+    uint32_t depth = 0, nt = 0;
     const float vx = ((R[0] * mx + R[1] * my) + R[2] * mz) + cam.t[0];
     const float vy = ((R[3] * mx + R[4] * my) + R[5] * mz) + cam.t[1];
     const float vz = ((R[6] * mx + R[7] * my) + R[8] * mz) + cam.t[2];
@@ -153,20 +156,25 @@ __global__ void __launch_bounds__(256) k1_project(const float4* __restrict__ po,
       const float b = (Qm[0][0] * T[1][0] + Qm[0][1] * T[1][1]) + Qm[0][2] * T[1][2];
       const float cc = ((Qm[1][0] * T[1][0] + Qm[1][1] * T[1][1]) + Qm[1][2] * T[1][2]) + kDilation;
       const float det = a * cc - b * b;
-      if (det > 0.0f) {
-        const float mid = 0.5f * (a + cc);
-        const float lam = mid + sqrtf(fmaxf(mid * mid - det, 0.0f));
-        const float r = ceilf(kRadiusK * sqrtf(lam));
-        const uint32_t x0 = (uint32_t)clampf(floorf((u - r) * 0.0625f), 0.0f, (float)gx);
-        const uint32_t x1 = (uint32_t)clampf(ceilf((u + r) * 0.0625f), 0.0f, (float)gx);
-        const uint32_t y0 = (uint32_t)clampf(floorf((v - r) * 0.0625f), 0.0f, (float)gy);
-        const uint32_t y1 = (uint32_t)clampf(ceilf((v + r) * 0.0625f), 0.0f, (float)gy);
-        const uint32_t ntt = (x1 - x0) * (y1 - y0);
+      // O1 step 14: pixel rows of the span extent
+      const float ye = sqrtf(kSpanT * cc) + kSpanM;
+      const float fpy0 = fmaxf(ceilf((v - ye) - 0.5f), 0.0f);
+      const float fpy1 = fminf(floorf((v + ye) - 0.5f), (float)(H - 1));
+      if (det > 0.0f && fpy0 <= fpy1) {
+        const float sp = b / cc, sh = det / cc, sic = 1.0f / cc, sdys = b * sqrtf(kSpanT / a);
+        const uint32_t py0 = (uint32_t)fpy0, py1 = (uint32_t)fpy1;
+        // O1 step 15: n_tiles = sum of the tile rows' span widths
+        uint32_t ntt = 0;
+        for (uint32_t r = py0 >> 4; r <= (py1 >> 4); ++r) {
+          uint32_t x0, x1;
+          row_span(u, v, sp, sh, sic, sdys, py0, py1, r, W, x0, x1);
+          ntt += x1 - x0;
+        }
         if (ntt > 0) {
           depth = __float_as_uint(vz);
-          xr = x0 | (x1 << 16);
-          yr = y0 | (y1 << 16);
           nt = ntt;
+          span[2 * cg] = make_uint4(__float_as_uint(u), __float_as_uint(v), __float_as_uint(sp), __float_as_uint(sh));
+          span[2 * cg + 1] = make_uint4(__float_as_uint(sic), __float_as_uint(sdys), py0 | (py1 << 16), ntt);
           const float inv = 1.0f / det;
           const float A = cc * inv, B = -(b * inv), C = a * inv;
           // SH colour
@@ -189,10 +197,8 @@ __global__ void __launch_bounds__(256) k1_project(const float4* __restrict__ po,
         }
       }
     }
-    bin[cg] = depth;
-    bin[VN + cg] = xr;
-    bin[2 * VN + cg] = yr;
-    bin[3 * VN + cg] = nt;
+    depth_plane[cg] = depth;
+    nt_plane[cg] = nt;
   }
 }
 
@@ -201,7 +207,6 @@ __global__ void __launch_bounds__(256) k1_project(const float4* __restrict__ po,
 cudaError_t launch_project(const gsr_gaussians& G, const CamBatch& cams, int V, float* rec, uint32_t* bin,
                            cudaStream_t st) {
   const int W = cams.c[0].width, H = cams.c[0].height;
-  const int gx = (W + kTile - 1) / kTile, gy = (H + kTile - 1) / kTile;
   const int64_t n = G.n;
   const unsigned blocks = (unsigned)((n + 255) / 256);
   auto po = reinterpret_cast<const float4*>(G.pos_opacity);
@@ -210,10 +215,10 @@ cudaError_t launch_project(const gsr_gaussians& G, const CamBatch& cams, int V, 
   auto sh = reinterpret_cast<const float4*>(G.sh);
   auto r4 = reinterpret_cast<float4*>(rec);
   switch (G.sh_degree) {
-    case 0: k1_project<0><<<blocks, 256, 0, st>>>(po, su, rq, sh, n, V, gx, gy, cams, r4, bin); break;
-    case 1: k1_project<1><<<blocks, 256, 0, st>>>(po, su, rq, sh, n, V, gx, gy, cams, r4, bin); break;
-    case 2: k1_project<2><<<blocks, 256, 0, st>>>(po, su, rq, sh, n, V, gx, gy, cams, r4, bin); break;
-    default: k1_project<3><<<blocks, 256, 0, st>>>(po, su, rq, sh, n, V, gx, gy, cams, r4, bin); break;
+    case 0: k1_project<0><<<blocks, 256, 0, st>>>(po, su, rq, sh, n, V, W, H, cams, r4, bin); break;
+    case 1: k1_project<1><<<blocks, 256, 0, st>>>(po, su, rq, sh, n, V, W, H, cams, r4, bin); break;
+    case 2: k1_project<2><<<blocks, 256, 0, st>>>(po, su, rq, sh, n, V, W, H, cams, r4, bin); break;
+    default: k1_project<3><<<blocks, 256, 0, st>>>(po, su, rq, sh, n, V, W, H, cams, r4, bin); break;
   }
   return cudaGetLastError();
 }

@@ -46,7 +46,7 @@ class _Slot:
         self.comp = comp if comp is not None else stream
         with torch.cuda.stream(stream):
             self.rec = torch.empty((V, max(n, 1), 12), dtype=torch.float32, device=dev)
-            self.bin = torch.empty((4, V, max(n, 1)), dtype=torch.int32, device=dev)
+            self.bin = torch.empty(10 * V * max(n, 1), dtype=torch.int32, device=dev)  # spans + depth + n_tiles
             self.n_frag = torch.zeros(2, dtype=torch.int64, device=dev)  # [blended, evaluated]
         self.capacity = 0
         self.vals = None
@@ -151,7 +151,7 @@ class ViewScorer:
         st = S.stream
         if S.comp is not S.stream:
             st.wait_stream(S.comp)  # the previous composite of this slot still reads rec / vals / ranges
-        # rec / bin hold [V][n][12] and [4][V][n] for THIS batch's V, packed from the
+        # rec / bin hold [V][n][12] and [10 V n] for THIS batch's V, packed from the
         # start of the (batch_views-sized) buffers: the base pointers are passed.
         gsr.gsr_project(S.ctx, self.field, cams, S.rec, S.bin, st)
         while True:

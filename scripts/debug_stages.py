@@ -30,13 +30,13 @@ def run(field, cams, label):
     T = V * ((W + 15) // 16) * ((H + 15) // 16)
     o = oracle_batch(field, cams, images=True)
     rec = torch.zeros((V, n, 12), device="cuda")
-    binr = torch.zeros((4, V, n), dtype=torch.int32, device="cuda")
+    binr = torch.zeros(10 * V * n, dtype=torch.int32, device="cuda")
     gsr.gsr_project(ctx, G, cams, rec, binr)
     torch.cuda.synchronize()
-    b = binr.cpu().numpy().view(np.uint32)
+    b = binr.cpu().numpy().view(np.uint32)[8 * V * n:].reshape(2, V, n)  # depth, n_tiles planes
     for v, p in enumerate(o["projs"]):
         if v < 2 or v == V - 1:
-            cmp(f"view{v} n_tiles", b[3, v], p["n_tiles"])
+            cmp(f"view{v} n_tiles", b[1, v], p["n_tiles"])
             cmp(f"view{v} depth", b[0, v], p["depth_bits"])
     K = len(o["keys"])
     print("  oracle K", K)

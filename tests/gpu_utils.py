@@ -19,7 +19,7 @@ def gpu_batch(ctx, field, cams, images=True, want_unsorted=True, want_keys=True)
     gx, gy = (W + 15) // 16, (H + 15) // 16
     T = V * gx * gy
     rec = torch.full((V, max(n, 1), 12), float("nan"), dtype=torch.float32, device="cuda")
-    binr = torch.full((4, V, max(n, 1)), -1, dtype=torch.int32, device="cuda")
+    binr = torch.full((10 * V * max(n, 1),), -1, dtype=torch.int32, device="cuda")
     gsr.gsr_project(ctx, G, cams, rec, binr)
     cap = 0
     vals = torch.empty(1, dtype=torch.int32, device="cuda")
@@ -46,7 +46,10 @@ def gpu_batch(ctx, field, cams, images=True, want_unsorted=True, want_keys=True)
     scores = torch.full((V,), float("nan"), dtype=torch.float32, device="cuda")
     gsr.gsr_score_views(ctx, partial, cams, scores)
     torch.cuda.synchronize()
-    out = dict(K=K, rec=rec.cpu().numpy(), bin=binr.cpu().numpy().view(np.uint32),
+    b = binr.cpu().numpy().view(np.uint32)
+    M = V * max(n, 1)
+    out = dict(K=K, rec=rec.cpu().numpy(), span=b[:8 * M].reshape(V, max(n, 1), 8),
+               depth=b[8 * M:9 * M].reshape(V, max(n, 1)), n_tiles=b[9 * M:].reshape(V, max(n, 1)),
                vals=vals.cpu().numpy().view(np.uint32)[:K], ranges=ranges.cpu().numpy().view(np.uint32),
                partial=partial.cpu().numpy(), scores=scores.cpu().numpy(), n_frag=int(nfrag[0].item()),
                n_eval=int(nfrag[1].item()))
@@ -84,14 +87,17 @@ def oracle_batch(field, cams, images=True):
 
 
 def check_projection(gpu, orc, n):
-    """Bin records bit-exact; render records bit-exact where visible."""
+    """Bin records (depth, n_tiles, span records) bit-exact; render records
+    bit-exact where visible."""
     for v, p in enumerate(orc["projs"]):
-        b = gpu["bin"][:, v, :n]
-        assert np.array_equal(b[3], p["n_tiles"]), f"view {v}: n_tiles"
-        assert np.array_equal(b[0], p["depth_bits"]), f"view {v}: depth"
-        assert np.array_equal(b[1] & 0xFFFF, p["x0"]) and np.array_equal(b[1] >> 16, p["x1"])
-        assert np.array_equal(b[2] & 0xFFFF, p["y0"]) and np.array_equal(b[2] >> 16, p["y1"])
+        assert np.array_equal(gpu["n_tiles"][v, :n], p["n_tiles"]), f"view {v}: n_tiles"
+        assert np.array_equal(gpu["depth"][v, :n], p["depth_bits"]), f"view {v}: depth"
         vis = p["n_tiles"] > 0
+        sp = gpu["span"][v, :n][vis]
+        for col, name in [(0, "u"), (1, "v"), (2, "sp_p"), (3, "sp_h"), (4, "sp_ic"), (5, "sp_dys")]:
+            assert np.array_equal(sp[:, col], p[name][vis].view(np.uint32)), f"view {v}: span {name}"
+        assert np.array_equal(sp[:, 6] & 0xFFFF, p["py0"][vis]) and np.array_equal(sp[:, 6] >> 16, p["py1"][vis])
+        assert np.array_equal(sp[:, 7], p["n_tiles"][vis]), f"view {v}: span n_tiles"
         r = gpu["rec"][v, :n][vis]
         for col, name in [(0, "u"), (1, "v"), (2, "A"), (3, "B"), (4, "C"), (5, "o"), (6, "unc"),
                           (8, "r"), (9, "g"), (10, "b")]:

@@ -174,23 +174,80 @@ def test_projection_culls():
     assert P["n_tiles"][4] > 0
 
 
-def test_rect_contains_every_visible_pixel():
-    """Every pixel with alpha >= 1/255 lies inside the Gaussian's tile rect
-    (brute-force scan of single-Gaussian images)."""
+def _span_test_gaussians(rng, cam, trials):
+    """Single Gaussians of every shape the spans must handle: tiny to large,
+    strongly anisotropic (one thin axis), any rotation, any opacity, centred
+    on and off screen."""
+    for trial in range(trials):
+        m = rng.uniform(-1.0, 1.0, (1, 3))
+        s = np.exp(rng.normal(-2.5, 0.9, (1, 3)))
+        if trial % 3 == 0:
+            s[0, rng.integers(0, 3)] *= 0.05
+        yield field_from(m, s, random_unit_quats(rng, 1), [rng.uniform(0.02, 1.0)], [[1, 1, 1]], [1])
+
+
+def _alpha64(p, W, H):
+    """float64 alpha = o exp(-q/2) at every pixel centre from the projected
+    conic (the conic itself is pinned by the projection tests above)."""
+    ys, xs = np.mgrid[0:H, 0:W]
+    dx = float(p["u"]) - (xs + 0.5)
+    dy = float(p["v"]) - (ys + 0.5)
+    q = float(p["A"]) * dx * dx + 2.0 * float(p["B"]) * dx * dy + float(p["C"]) * dy * dy
+    return float(p["o"]) * np.exp(-0.5 * q), q
+
+
+def test_spans_contain_every_visible_pixel():
+    """Lossless tiling (O1 step 15): every pixel whose alpha >= 1/255
+    -- in the brute-force composite AND in float64 real arithmetic from the
+    conic -- lies in a tile the Gaussian's spans emit."""
     rng = np.random.default_rng(3)
     cam = synth.look_at([0.0, 0.3, -3.0], [0, 0, 0], 72, 56, 70.0)
-    for trial in range(40):
-        m = rng.uniform(-0.8, 0.8, (1, 3))
-        s = np.exp(rng.normal(-2.3, 0.6, (1, 3)))
-        fld = field_from(m, s, random_unit_quats(rng, 1), [rng.uniform(0.05, 1.0)], [[1, 1, 1]], [1])
+    W, H = 72, 56
+    n_vis = 0
+    for fld in _span_test_gaussians(rng, cam, 120):
         p = oracle.project(fld, cam)
         img = oracle.composite_brute(p, cam)
         ys, xs = np.nonzero(img["n_contrib"])
         if p[0]["n_tiles"] == 0:
             assert len(xs) == 0
             continue
-        tx, ty = xs // 16, ys // 16
-        assert np.all((tx >= p[0]["x0"]) & (tx < p[0]["x1"]) & (ty >= p[0]["y0"]) & (ty < p[0]["y1"]))
+        n_vis += 1
+        tiles = set(oracle.tiles_of(p[0], cam))
+        assert len(tiles) == int(p[0]["n_tiles"])
+        assert all((y // 16, x // 16) in tiles for y, x in zip(ys, xs))
+        a64, _ = _alpha64(p[0], W, H)
+        ys, xs = np.nonzero(a64 >= (1.0 / 255.0) * (1.0 - 1e-6))
+        assert all((y // 16, x // 16) in tiles for y, x in zip(ys, xs))
+    assert n_vis > 60
+
+
+def test_spans_are_tight():
+    """Every emitted tile holds a pixel centre within (m + 1e-3) px of the
+    ellipse q <= 11.1: q64 <= (sqrt(11.1) + (m + 1e-3) / sqrt(lambda_min(Sigma')))^2
+    (float64 eigenvalues of the covariance = inverse conic).  Tiles of the
+    3.33-sigma square box that only the box reaches are not emitted."""
+    rng = np.random.default_rng(4)
+    cam = synth.look_at([0.2, 0.5, -2.6], [0, 0, 0], 80, 64, 75.0)
+    W, H = 80, 64
+    saved = 0
+    for fld in _span_test_gaussians(rng, cam, 120):
+        p = oracle.project(fld, cam)[0]
+        if p["n_tiles"] == 0:
+            continue
+        conic = np.array([[p["A"], p["B"]], [p["B"], p["C"]]], dtype=np.float64)
+        lam_min = np.linalg.eigvalsh(np.linalg.inv(conic))[0]
+        qmax = (math.sqrt(11.1) + (0.0625 + 1e-3) / math.sqrt(lam_min)) ** 2
+        _, q = _alpha64(p, W, H)
+        for ty, tx in oracle.tiles_of(p, cam):
+            assert q[16 * ty:16 * ty + 16, 16 * tx:16 * tx + 16].min() <= qmax, (ty, tx)
+        # the square box of radius ceil(3.33 sqrt(lambda_max)) (SURVEY §8(c) O1 step 14)
+        r = math.ceil(3.33 * math.sqrt(np.linalg.eigvalsh(np.linalg.inv(conic))[1]))
+        bx = (min(max(math.floor((p["u"] - r) / 16), 0), 5), min(max(math.ceil((p["u"] + r) / 16), 0), 5))
+        by = (min(max(math.floor((p["v"] - r) / 16), 0), 4), min(max(math.ceil((p["v"] + r) / 16), 0), 4))
+        box = (bx[1] - bx[0]) * (by[1] - by[0])
+        assert p["n_tiles"] <= box
+        saved += box - int(p["n_tiles"])
+    assert saved > 0
 
 
 # ----------------------------------------------------------------------------- keys / sort / ranges
@@ -203,7 +260,7 @@ def _small_batch(seed=0, n=400, W=48, H=40, views=3, deg=1):
 def test_keys_emission_brute_force_enumeration():
     """O2 emission equals a brute-force enumeration over all (view, g, tile)
     triples of the batch grid, tested against each tile's membership in the
-    Gaussian's rect; key = (view*gx*gy + ty*gx + tx) << 32 | depth bits."""
+    Gaussian's spans; key = (view*gx*gy + ty*gx + tx) << 32 | depth bits."""
     fld, cams, projs = _small_batch()
     gx, gy = oracle.grid(cams[0])
     bs = oracle.bin_sort_batch(projs, cams)
@@ -212,9 +269,10 @@ def test_keys_emission_brute_force_enumeration():
         for g in range(len(p)):
             if p[g]["n_tiles"] == 0:
                 continue
+            member = set(oracle.tiles_of(p[g], cams[v]))
             for tile in range(gx * gy):
                 ty, tx = divmod(tile, gx)
-                if p[g]["x0"] <= tx < p[g]["x1"] and p[g]["y0"] <= ty < p[g]["y1"]:
+                if (ty, tx) in member:
                     exp_k.append(((v * gx * gy + tile) << 32) | int(p[g]["depth_bits"]))
                     exp_v.append(g)
     assert bs["keys_unsorted"].tolist() == exp_k
@@ -361,7 +419,7 @@ def test_termination_stops_before_blending():
 @pytest.mark.parametrize("seed,deg", [(0, 0), (1, 1), (2, 2), (3, 3), (4, 3)])
 def test_brute_force_equals_tiled_bit_exact(seed, deg):
     """Tiled (per-tile sorted lists) == brute force (all Gaussians, global depth
-    order) bit for bit: entries outside a Gaussian's rect take the alpha < 1/255
+    order) bit for bit: pixels outside a Gaussian's spans take the alpha < 1/255
     skip, so both loops perform identical state updates.  48x40 image = 3x3 tiles
     with ragged right/bottom tiles."""
     fld, cams = synth.random_scene_small(seed, 300, 48, 40, 45.0, 2, deg, logscale_mu=-2.2)
@@ -377,10 +435,10 @@ def test_brute_force_equals_tiled_bit_exact(seed, deg):
 
 @pytest.mark.parametrize("u,probe,visible", [(17.0, 32, True), (31.0, 48, False)])
 def test_edge_aligned_box_is_lossless(u, probe, visible):
-    """SURVEY §8(c) k row: isotropic Sigma' = 25 I, o = 0.99.  At u = 17 the
+    """SURVEY §8(c) k row: isotropic Sigma' = 25 I, o = 0.99.  At u = 17 a
     k = 3 box (r = 15) would stop at pixel 31 but pixel 32 has alpha = 0.0081 >=
-    1/255; with k = 3.33 (r = 17) tiling keeps it.  At u = 31 pixel 48 (first
-    pixel past the k = 3.33 box) has alpha = 0.0022 < 1/255."""
+    1/255; the q <= 11.1 spans (x-extent 16.66 px) keep it.  At u = 31 pixel 48
+    (first pixel past the span, tile 3) has alpha = 0.0022 < 1/255."""
     f, D = 100.0, 2.0
     sig = D * math.sqrt(24.7) / f
     cam = axis_camera(80, 16, f, cx=u, cy=8.5)
