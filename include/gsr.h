@@ -160,6 +160,8 @@ gsr_status gsr_bin_sort(gsr_ctx* ctx, const uint32_t* bin_rec, int64_t n, const 
    render_rec, n, vals, ranges: as produced above for the same batch
    rgbu        OPTIONAL [V][H][W][4] float (r, g, b, U)
    t_final     OPTIONAL [V][H][W] float;   n_contrib OPTIONAL [V][H][W] uint32
+   gray        OPTIONAL [V][H][W] float: ((r + g) + b) / 3 of the composited pixel,
+               the input of gsr_sobel_scores (NEXT-4)
    tile_partial [V][gx*gy] float: sum of U over the tile's in-image pixels
    n_frag      OPTIONAL [2] uint64, ADDED to: [0] blended (pixel, Gaussian) pairs
                ("composited fragments"); [1] (pixel, list entry) pairs the plain
@@ -167,8 +169,8 @@ gsr_status gsr_bin_sort(gsr_ctx* ctx, const uint32_t* bin_rec, int64_t n, const 
                including the one that stops it (the whole list if none does) */
 gsr_status gsr_composite(gsr_ctx* ctx, const float* render_rec, int64_t n, const uint32_t* vals,
                          const uint32_t* ranges, const gsr_camera* cams, int32_t n_views,
-                         float* rgbu, float* t_final, uint32_t* n_contrib, float* tile_partial,
-                         unsigned long long* n_frag, void* stream);
+                         float* rgbu, float* t_final, uint32_t* n_contrib, float* gray,
+                         float* tile_partial, unsigned long long* n_frag, void* stream);
 
 /* ---- K7: view score u(θ) = (sum of U over all W*H pixels) / (W*H) ----------
    (north_star "mean composited uncertainty"; the paper's spatial means
@@ -186,6 +188,19 @@ gsr_status gsr_score_views(gsr_ctx* ctx, const float* tile_partial, const gsr_ca
    (device).  n <= 16384.  GSR_EBUDGET if k < 1 or k > n - #excluded. */
 gsr_status gsr_select_nbv(gsr_ctx* ctx, const float* scores, int32_t n, const uint8_t* exclude,
                           int32_t k, int32_t* out_idx, void* stream);
+
+/* ---- NEXT-4: image-space spatial-frequency term of eq:uncert_img -----------
+   (§3.3: "grad is computed using a 3x3 Sobel operator and
+   the result is reduced to a scalar via per-pixel Euclidean norm and global
+   average"; the image is the rendered view, grayscale = channel mean, with
+   replicate padding as SPEC sobel_gradient_scalar S:L241-248 reads it).
+   scores[v] = (1/(W H)) sum_p sqrt(Sx(p)^2 + Sy(p)^2) over the gray image.
+   gray         [V][H][W] float (gsr_composite's gray output)
+   tile_partial [V][gx*gy] float scratch (per-tile sums of magnitudes)
+   scores       [V] float.  EINVAL unless W, H >= 3 and 1 <= V <= GSR_MAX_VIEWS.
+   The LPIPS term (pretrained AlexNet) is out of scope. */
+gsr_status gsr_sobel_scores(gsr_ctx* ctx, const float* gray, const gsr_camera* cams, int32_t n_views,
+                            float* tile_partial, float* scores, void* stream);
 
 /* ---- NEXT-1: latent-space ensemble disagreement (PAPER.md eq:w2_pixel,
    §3.3) ---------------------------------------------------------------
@@ -226,7 +241,8 @@ enum {
   GSR_STAGE_SELECT = 8,     /* K8 */
   GSR_STAGE_SORT_U64 = 9,   /* utility sort (histogram + passes) */
   GSR_STAGE_W2 = 10,        /* NEXT-1 latent W2 scorer */
-  GSR_N_STAGES = 11
+  GSR_STAGE_SOBEL = 11,     /* NEXT-4 Sobel image term */
+  GSR_N_STAGES = 12
 };
 /* enable != 0: bracket every stage with CUDA events on its launch stream. */
 gsr_status gsr_timing_enable(gsr_ctx* ctx, int enable);

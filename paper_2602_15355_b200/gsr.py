@@ -31,9 +31,10 @@ assert CAM_DTYPE.itemsize == 96
 
 EXPORTED = ["gsr_create", "gsr_destroy", "gsr_last_error", "gsr_version", "gsr_camera_look_at",
             "gsr_project", "gsr_bin_sort", "gsr_composite", "gsr_score_views", "gsr_select_nbv",
-            "gsr_sort_pairs_u64", "gsr_scratch_bytes", "gsr_timing_enable", "gsr_timing_read", "gsr_w2_scores"]
+            "gsr_sort_pairs_u64", "gsr_scratch_bytes", "gsr_timing_enable", "gsr_timing_read", "gsr_w2_scores",
+            "gsr_sobel_scores"]
 STAGES = ["project", "compact", "depth_sort", "emit", "ranges", "tile_sort", "composite", "score", "select",
-          "sort_u64", "w2"]
+          "sort_u64", "w2", "sobel"]
 
 
 class GsrError(RuntimeError):
@@ -62,7 +63,8 @@ def _load():
     L.gsr_camera_look_at.argtypes = [ctypes.c_double] * 3 + [P, i32, i32, ctypes.c_double, ctypes.c_double, P]
     L.gsr_project.argtypes = [P, P, P, i32, P, P, P]
     L.gsr_bin_sort.argtypes = [P, P, i64, P, i32, P, P, i64, P, P, P, P, P]
-    L.gsr_composite.argtypes = [P, P, i64, P, P, P, i32, P, P, P, P, P, P]
+    L.gsr_composite.argtypes = [P, P, i64, P, P, P, i32, P, P, P, P, P, P, P]
+    L.gsr_sobel_scores.argtypes = [P, P, P, i32, P, P, P]
     L.gsr_score_views.argtypes = [P, P, P, i32, P, P]
     L.gsr_select_nbv.argtypes = [P, P, i32, P, i32, P, P]
     L.gsr_sort_pairs_u64.argtypes = [P, P, P, P, P, i64, i32, i32, P]
@@ -200,11 +202,18 @@ def gsr_bin_sort(ctx: Context, bin_rec, n: int, cams, vals, capacity: int, range
 
 
 def gsr_composite(ctx: Context, render_rec, n: int, vals, ranges, cams, tile_partial, rgbu=None, t_final=None,
-                  n_contrib=None, n_frag=None, stream=None):
+                  n_contrib=None, n_frag=None, gray=None, stream=None):
     c = cams_array(cams)
     ctx._check(lib.gsr_composite(ctx.handle, _ptr(render_rec), n, _ptr(vals), _ptr(ranges), c.ctypes.data, len(c),
-                                 _ptr(rgbu), _ptr(t_final), _ptr(n_contrib), _ptr(tile_partial), _ptr(n_frag),
-                                 _stream(stream)))
+                                 _ptr(rgbu), _ptr(t_final), _ptr(n_contrib), _ptr(gray), _ptr(tile_partial),
+                                 _ptr(n_frag), _stream(stream)))
+
+
+def gsr_sobel_scores(ctx: Context, gray, cams, tile_partial, scores, stream=None):
+    """NEXT-4 (PAPER.md eq:uncert_img): mean Sobel gradient magnitude of gray [V][H][W]."""
+    c = cams_array(cams)
+    ctx._check(lib.gsr_sobel_scores(ctx.handle, _ptr(gray), c.ctypes.data, len(c), _ptr(tile_partial), _ptr(scores),
+                                    _stream(stream)))
 
 
 def gsr_score_views(ctx: Context, tile_partial, cams, scores, stream=None):

@@ -53,6 +53,8 @@ class _Slot:
         self.keys = None
         self.ranges = None
         self.partial = None
+        self.gray = None      # NEXT-4: [V][H][W] gray image of the batch
+        self.partial2 = None  # NEXT-4: per-tile Sobel sums
 
 
 class ViewScorer:
@@ -137,8 +139,17 @@ class ViewScorer:
         caller.wait_stream(S.comp)
         return out
 
+    @staticmethod
+    def _ensure_gray(slot: _Slot, V: int, H: int, W: int, T: int):
+        if slot.gray is None or slot.gray.numel() < V * H * W:
+            with torch.cuda.stream(slot.stream):
+                slot.gray = torch.empty(V * H * W, dtype=torch.float32, device=slot.rec.device)
+        if slot.partial2 is None or slot.partial2.numel() < T:
+            with torch.cuda.stream(slot.stream):
+                slot.partial2 = torch.empty(T, dtype=torch.float32, device=slot.rec.device)
+
     def _enqueue(self, S: _Slot, cams, scores_out, images=None, t_final=None, n_contrib=None,
-                 want_keys: bool = False) -> BatchOut:
+                 want_keys: bool = False, sobel_out=None) -> BatchOut:
         cams = gsr.cams_array(cams)
         V = len(cams)
         assert 0 < V <= self.V
@@ -166,15 +177,25 @@ class ViewScorer:
         cs = S.comp
         if cs is not st:
             cs.wait_stream(st)
+        gray = None
+        if sobel_out is not None:
+            W, H = int(cams[0]["width"]), int(cams[0]["height"])
+            self._ensure_gray(S, V, H, W, V * tiles_per_view(cams[0]))
+            gray = S.gray
         gsr.gsr_composite(S.ctx, S.rec, n, S.vals, S.ranges, cams, S.partial, rgbu=images, t_final=t_final,
-                          n_contrib=n_contrib, n_frag=S.n_frag, stream=cs)
+                          n_contrib=n_contrib, n_frag=S.n_frag, gray=gray, stream=cs)
         gsr.gsr_score_views(S.ctx, S.partial, cams, scores_out, cs)
+        if sobel_out is not None:
+            gsr.gsr_sobel_scores(S.ctx, gray, cams, S.partial2, sobel_out, cs)
         return BatchOut(K, images)
 
-    def score_views(self, cams: np.ndarray, scores_out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    def score_views(self, cams: np.ndarray, scores_out: Optional[torch.Tensor] = None,
+                    sobel_out: Optional[torch.Tensor] = None) -> torch.Tensor:
         """Scores for all of ``cams`` (any count; same resolution), batches
         alternating over the slots' streams; the result is ordered back onto
-        the caller's current stream."""
+        the caller's current stream.  ``sobel_out`` (optional [len(cams)]
+        float tensor) also receives the NEXT-4 image term (mean Sobel
+        gradient magnitude of each rendered view, PAPER.md eq:uncert_img)."""
         cams = gsr.cams_array(cams)
         if scores_out is None:
             scores_out = torch.empty(len(cams), dtype=torch.float32, device=self.dev)
@@ -185,7 +206,8 @@ class ViewScorer:
         self.last_keys = []
         for i, b0 in enumerate(range(0, len(cams), self.V)):
             b1 = min(len(cams), b0 + self.V)
-            out = self._enqueue(self.slots[i % len(self.slots)], cams[b0:b1], scores_out[b0:b1])
+            out = self._enqueue(self.slots[i % len(self.slots)], cams[b0:b1], scores_out[b0:b1],
+                                sobel_out=None if sobel_out is None else sobel_out[b0:b1])
             self.last_keys.append(out.n_keys)
         for s in self.slots:
             caller.wait_stream(s.comp)

@@ -10,7 +10,7 @@ def to_dev(field):
     return Gaussians(torch.from_numpy(np.ascontiguousarray(field.planes)).cuda(), field.sh_degree)
 
 
-def gpu_batch(ctx, field, cams, images=True, want_unsorted=True, want_keys=True):
+def gpu_batch(ctx, field, cams, images=True, want_unsorted=True, want_keys=True, want_gray=False):
     """One batch (len(cams) <= 64, same W,H) through K1..K7; numpy outputs."""
     from paper_2602_15355_b200 import gsr
     G = to_dev(field)
@@ -42,7 +42,9 @@ def gpu_batch(ctx, field, cams, images=True, want_unsorted=True, want_keys=True)
     tf = torch.full((V, H, W), float("nan"), dtype=torch.float32, device="cuda") if images else None
     nc = torch.full((V, H, W), -1, dtype=torch.int32, device="cuda") if images else None
     nfrag = torch.zeros(2, dtype=torch.int64, device="cuda")
-    gsr.gsr_composite(ctx, rec, n, vals, ranges, cams, partial, rgbu=rgbu, t_final=tf, n_contrib=nc, n_frag=nfrag)
+    gray = torch.full((V, H, W), float("nan"), dtype=torch.float32, device="cuda") if want_gray else None
+    gsr.gsr_composite(ctx, rec, n, vals, ranges, cams, partial, rgbu=rgbu, t_final=tf, n_contrib=nc, n_frag=nfrag,
+                      gray=gray)
     scores = torch.full((V,), float("nan"), dtype=torch.float32, device="cuda")
     gsr.gsr_score_views(ctx, partial, cams, scores)
     torch.cuda.synchronize()
@@ -58,6 +60,8 @@ def gpu_batch(ctx, field, cams, images=True, want_unsorted=True, want_keys=True)
     if want_unsorted:
         out["keys_unsorted"] = ku.cpu().numpy().view(np.uint64)[:K]
         out["vals_unsorted"] = vu.cpu().numpy().view(np.uint32)[:K]
+    if want_gray:
+        out["gray"] = gray.cpu().numpy()
     if images:
         out.update(rgbu=rgbu.cpu().numpy(), t_final=tf.cpu().numpy(), n_contrib=nc.cpu().numpy().view(np.uint32))
     return out
