@@ -184,6 +184,36 @@ def bench_w2(gsr, dev, peaks, reps: int = 20):
                          "unit": "GB/s", "frac": round(byts / t / 1e9 / peaks["hbm_gbs"], 4)}}
 
 
+def bench_sobel(gsr, dev, peaks, reps: int = 20):
+    """NEXT-4: Sobel image term (PAPER.md eq:uncert_img) over the gray images of
+    one 16-view c3 batch (800 x 800), HBM roofline on the 4 B read per pixel
+    (the 18 x 18 halo re-reads hit L2) + 4 B per tile partial."""
+    import torch
+    import synth
+    V, W, H = 16, 800, 800
+    g = torch.rand((V, H, W), device=dev)
+    cams = synth.fibonacci_cameras(V, 4.0, W, H, 900.0)
+    tpv = ((W + 15) // 16) * ((H + 15) // 16)
+    part = torch.empty(V * tpv, device=dev)
+    sc = torch.empty(V, device=dev)
+    ctx = gsr.Context(dev.index or 0)
+    for _ in range(3):
+        gsr.gsr_sobel_scores(ctx, g, cams, part, sc)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        gsr.gsr_sobel_scores(ctx, g, cams, part, sc)
+    e1.record()
+    torch.cuda.synchronize()
+    t = e0.elapsed_time(e1) / reps / 1e3
+    byts = 4.0 * V * W * H + 8.0 * V * tpv
+    return {"metric": "sobel_views_scored_per_sec", "value": round(V / t, 1), "unit": "views/s",
+            "ms_per_batch": round(t * 1e3, 4), "config": "16 views x 800x800 gray (c3 resolution)",
+            "roofline": {"bound": "hbm", "achieved": round(byts / t / 1e9, 1), "peak": peaks["hbm_gbs"],
+                         "unit": "GB/s", "frac": round(byts / t / 1e9 / peaks["hbm_gbs"], 4)}}
+
+
 # ----------------------------------------------------------------------------- GPU arm
 def main():
     args = parse()
@@ -313,9 +343,9 @@ def main():
     comp_t = st_ms["composite"] / 1e3
     ach_ops = comp_ops / comp_t / 1e12
     n_comp = max(1, stages["composite"]["launches"] // args.steps)
-    roof = {"bound": "alu", "kernel": "k6_composite_v2", "achieved": round(ach_ops, 2), "peak": round(peak_ops, 2),
+    roof = {"bound": "alu", "kernel": "k6_composite", "achieved": round(ach_ops, 2), "peak": round(peak_ops, 2),
             "unit": "Top/s", "frac": round(ach_ops / peak_ops, 4),
-            "traffic": traffic.get("k6_composite_v2"),
+            "traffic": traffic.get("k6_composite"),
             "work": "28 FP32 ops per (pixel, list entry) pair the plain definition evaluates + 8 per blended "
                     "fragment, per launch = 16 views",
             "peak_source": f"148 SMs x 128 FP32 lanes x {f_clk / 1e6:.0f} MHz (median SM clock under load)",
@@ -339,6 +369,7 @@ def main():
             "keys_per_step_rank0": int(sum(scorer.last_keys))}
     if rank == 0:
         line["next1_w2"] = bench_w2(gsr, dev, peaks)
+        line["next4_sobel"] = bench_sobel(gsr, dev, peaks)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(scene, args.cpu_views)
     if rank == 0:

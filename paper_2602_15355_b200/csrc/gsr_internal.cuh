@@ -17,7 +17,6 @@ namespace gsr {
 
 // ---- rasterizer constants (float32 hex in comments) ----
 constexpr float kDilation = 0.3f;          // 0x3e99999a  EWA low-pass, px^2
-constexpr float kRadiusK = 3.33f;          // 0x40551eb8  >= sqrt(2 ln 255) = 3.3290
 constexpr float kAlphaMax = 0.99f;         // 0x3f7d70a4
 constexpr float kTStop = 1e-4f;            // 0x38d1b717
 constexpr uint32_t kAlphaMinBits = 0x3b808081u;  // 1/255

@@ -69,8 +69,6 @@ __device__ __forceinline__ void sh_colour(const ShCoef<DEG>& S, float x, float y
   }
 }
 
-__device__ __forceinline__ float clampf(float v, float lo, float hi) { return fminf(fmaxf(v, lo), hi); }
-
 template <int DEG>
 __global__ void __launch_bounds__(256) k1_project(const float4* __restrict__ po, const float4* __restrict__ su,
                                                   const float4* __restrict__ rq, const float4* __restrict__ sh,
