@@ -47,6 +47,7 @@ def parse():
     p.add_argument("--cpu-views", type=int, default=0, help="oracle sample size (0 = auto)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-extras", action="store_true", help="skip the NEXT-1/2/4 extra measurements")
     return p.parse_args()
 
 
@@ -214,6 +215,45 @@ def bench_sobel(gsr, dev, peaks, reps: int = 20):
                          "unit": "GB/s", "frac": round(byts / t / 1e9 / peaks["hbm_gbs"], 4)}}
 
 
+def bench_lod(dev, steps: int = 3):
+    """NEXT-2: LOD blending (PAPER.md eq:lod_blend) on the config-4 fly-over
+    (64 views, 1920x1080): the 4x4 Wang assembly with six LOD levels per tile
+    (10.7 M Gaussians, K1 scales opacities by the level weights and culls the
+    inactive levels) vs the level-0-only assembly (8 M Gaussians, configs[3])."""
+    import torch
+    import synth
+    from paper_2602_15355_b200 import Gaussians, Lod
+    from paper_2602_15355_b200.pipeline import ViewScorer
+    cams = synth.flyover_cameras(64, 1920, 1080, 1500.0)
+    out = {"config": "c4 fly-over 64 views 1920x1080; LOD: 6 levels/tile (1/4 count, 2.3x scale per level), "
+                      "D = 1.5, 3, 6, 12, 24, delta = 0.25"}
+
+    def run(fld, lod):
+        G = Gaussians(torch.from_numpy(fld.planes).to(dev), fld.sh_degree)
+        L = None if lod is None else Lod(torch.from_numpy(lod.tile_level).to(dev), lod.levels, lod.delta,
+                                         lod.thresholds)
+        sc = ViewScorer(G, batch_views=16, n_slots=2, lod=L)
+        for _ in range(2):
+            sc.score_views(cams)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(steps):
+            sc.score_views(cams)
+        e1.record()
+        torch.cuda.synchronize()
+        t = e0.elapsed_time(e1) / steps / 1e3
+        return {"gaussians": fld.n, "views_per_sec": round(64 / t, 1), "ms_per_pass": round(t * 1e3, 2),
+                "keys_per_view": int(sum(sc.last_keys) / 64)}
+
+    fld, lod = synth.gen_config4_lod(500_000)
+    out["lod"] = run(fld, lod)
+    del fld, lod
+    out["level0_only"] = run(synth.gen_config4_field(500_000), None)
+    torch.cuda.empty_cache()
+    return out
+
+
 # ----------------------------------------------------------------------------- GPU arm
 def main():
     args = parse()
@@ -367,9 +407,10 @@ def main():
             "stages": stage_tab,
             "gpu_launches": int(launches * world), "clocks": clk, "e2e": e2e,
             "keys_per_step_rank0": int(sum(scorer.last_keys))}
-    if rank == 0:
+    if rank == 0 and not args.no_extras:
         line["next1_w2"] = bench_w2(gsr, dev, peaks)
         line["next4_sobel"] = bench_sobel(gsr, dev, peaks)
+        line["next2_lod"] = bench_lod(dev)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(scene, args.cpu_views)
     if rank == 0:

@@ -72,6 +72,24 @@ typedef struct {
   const float* sh;
 } gsr_gaussians;
 
+/* NEXT-2: continuous LOD blending (§3.5 eq:lod_blend L124-127, clamped
+   form of App. A.4).  Each Gaussian belongs to one LOD level of one
+   tile; at camera distance d = |campos - tile centre| its opacity is scaled by
+     w = min(fade_out, fade_in),
+     a(d, D)  = min(1, max(0, 0.5 - (d - D) / (2 delta)))      (eq:lod_blend)
+     fade_out = a(d, D_level)           (1 for the coarsest level)
+     fade_in  = 1 - a(d, D_{level-1})   (1 for level 0)
+   i.e. level i fades out around D_i while level i+1 fades in with the
+   complement (DESIGN.md reading; SPEC lod-cache S:L563-591).  A Gaussian
+   whose scaled opacity o w < 1/255 is culled (it can never reach alpha >=
+   1/255).  float32, evaluated in exactly this order on both sides. */
+typedef struct {
+  int32_t levels;          /* 1..8 */
+  float delta;             /* blending bandwidth > 0 */
+  float thresholds[7];     /* D_0 < D_1 < ... < D_{levels-2} (world units) */
+  const float* tile_level;  /* DEVICE [n][4]: (tile centre x, y, z, level as float) */
+} gsr_lod;
+
 /* One pinhole camera, world->camera, OpenCV axes (x right, y down, z forward).
    Built on the host in double and rounded once (gsr_camera_look_at).
    limx = 1.3 (W/2)/fx and limy = 1.3 (H/2)/fy are the EWA FOV clamp. 96 bytes. */
@@ -117,6 +135,9 @@ gsr_status gsr_camera_look_at(double elevation, double azimuth, double radius, c
    clipped to the image.  n_tiles = sum of span widths (0 = culled).
    cams        [host] n_views cameras, all with the same W,H (n_views <= GSR_MAX_VIEWS;
                W, H <= 65535)
+   lod         OPTIONAL LOD blending (see gsr_lod): opacity o -> o w before every
+               other step; EINVAL if levels not in [1,8], delta <= 0, thresholds
+               not increasing or tile_level NULL
    render_rec  [V][n][12] float: (u, v, A, B), (C, opacity, uncertainty, tau),
                (r, g, b, ext) -- conic (A,B,C) = inverse 2D covariance; tau =
                -ln(255 opacity) - 1e-3 (alpha-skip pre-test bound); ext = two
@@ -128,7 +149,8 @@ gsr_status gsr_camera_look_at(double elevation, double azimuth, double radius, c
                words [8Vn, 9Vn): depth bits of view-space z [V][n] (0 when culled);
                words [9Vn, 10Vn): n_tiles [V][n] (0 = culled). */
 gsr_status gsr_project(gsr_ctx* ctx, const gsr_gaussians* gaussians, const gsr_camera* cams,
-                       int32_t n_views, float* render_rec, uint32_t* bin_rec, void* stream);
+                       int32_t n_views, const gsr_lod* lod /* OPTIONAL [host] struct, NULL = off */,
+                       float* render_rec, uint32_t* bin_rec, void* stream);
 
 /* ---- K2-K5: tile-count scan, key duplication, radix sort, tile ranges ----
    Produces the (view, tile)-sorted Gaussian lists of the batch.  Key of a

@@ -40,6 +40,21 @@ assert PROJ_DTYPE.itemsize == 72
 TILE = 16
 
 
+class _Lod(ctypes.Structure):
+    """orc_lod: NEXT-2 LOD blending parameters (PAPER.md eq:lod_blend)."""
+    _fields_ = [("levels", ctypes.c_int32), ("delta", ctypes.c_float), ("thresholds", ctypes.c_float * 7),
+                ("tile_level", ctypes.c_void_p)]
+
+
+def _lod(lod):
+    """(ctypes struct or None, keep-alive array) from a synth.LodData (or None)."""
+    if lod is None:
+        return None, None
+    tl = np.ascontiguousarray(lod.tile_level, dtype=np.float32)
+    th = (ctypes.c_float * 7)(*[float(x) for x in list(lod.thresholds) + [0.0] * (7 - len(lod.thresholds))])
+    return _Lod(int(lod.levels), float(lod.delta), th, tl.ctypes.data), tl
+
+
 def build(force: bool = False) -> str:
     """Compile the oracle with gcc (no fast-math, no FMA contraction)."""
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
@@ -61,7 +76,11 @@ def lib():
         L.orc_exp_spec.argtypes = [ctypes.c_float]
         L.orc_exp_spec.restype = ctypes.c_float
         L.orc_sh_basis.argtypes = [ctypes.c_float] * 3 + [P]
-        L.orc_project.argtypes = [P, i64, ctypes.c_int, P, P]
+        L.orc_project.argtypes = [P, i64, ctypes.c_int, P, P, P]
+        L.orc_lod_blend.argtypes = [ctypes.c_float, ctypes.c_float, ctypes.c_float]
+        L.orc_lod_blend.restype = ctypes.c_float
+        L.orc_lod_weight.argtypes = [ctypes.c_float, ctypes.c_int, P]
+        L.orc_lod_weight.restype = ctypes.c_float
         L.orc_row_span.argtypes = [P, ctypes.c_uint32, ctypes.c_int, P, P]
         L.orc_count_keys.argtypes = [P, i64]
         L.orc_count_keys.restype = i64
@@ -72,7 +91,7 @@ def lib():
         L.orc_composite_tiled.restype = ctypes.c_double
         L.orc_composite_brute.argtypes = [P, i64, P, P, P, P, P]
         L.orc_composite_brute.restype = ctypes.c_double
-        L.orc_render_views.argtypes = [P, i64, ctypes.c_int, P, i32, ctypes.c_int, P, P, P, P]
+        L.orc_render_views.argtypes = [P, i64, ctypes.c_int, P, i32, P, ctypes.c_int, P, P, P, P]
         _lib = L
     return _lib
 
@@ -112,14 +131,27 @@ def sh_basis(d):
     return out
 
 
-def project(field, cam) -> np.ndarray:
-    """O1 + O4 for every Gaussian of ``field`` in one camera -> PROJ_DTYPE [n]."""
+def project(field, cam, lod=None) -> np.ndarray:
+    """O1 + O4 for every Gaussian of ``field`` in one camera -> PROJ_DTYPE [n]
+    (``lod``: optional synth.LodData, NEXT-2 opacity blending)."""
     L = lib()
     planes = np.ascontiguousarray(field.planes, dtype=np.float32)
     c = _cam(cam)
     out = np.zeros(field.n, dtype=PROJ_DTYPE)
-    L.orc_project(_p(planes), field.n, field.sh_degree, _p(c), _p(out))
+    ls, keep = _lod(lod)
+    L.orc_project(_p(planes), field.n, field.sh_degree, _p(c), ctypes.byref(ls) if ls else None, _p(out))
     return out
+
+
+def lod_blend(d, D, delta):
+    """eq:lod_blend, clamped (App. A.4): max(0, min(1, 0.5 - (d - D) / (2 delta)))."""
+    return float(lib().orc_lod_blend(float(d), float(D), float(delta)))
+
+
+def lod_weight(d, level, lod):
+    """Opacity multiplier of a level-``level`` Gaussian at camera distance d."""
+    ls, keep = _lod(lod)
+    return float(lib().orc_lod_weight(float(d), int(level), ctypes.byref(ls)))
 
 
 def row_span(proj_one, ty: int, cam):
@@ -219,17 +251,17 @@ def composite_brute(proj, cam):
     return dict(rgbu=rgbu, t_final=tf, n_contrib=nc, score=score, n_frag=int(nf[0]), n_eval=int(nf[1]))
 
 
-def render_view(field, cam):
+def render_view(field, cam, lod=None):
     """O1..O6 for one view through the tiled path; returns a dict with the
     projection, bin-sort outputs, images and score."""
-    p = project(field, cam)
+    p = project(field, cam, lod)
     bs = bin_sort_batch([p], np.asarray([cam]))
     out = composite_tiled(p, bs["vals"], bs["ranges"], cam)
     out.update(proj=p, **bs)
     return out
 
 
-def render_views(field, cams, n_threads: int = 0, images: bool = False):
+def render_views(field, cams, n_threads: int = 0, images: bool = False, lod=None):
     """O1..O6 for many views, one view per host thread (bench cpu_baseline).
     Returns (scores float64 [V], n_frag uint64 [V], n_keys int64 [V], rgbu or None)."""
     L = lib()
@@ -246,8 +278,9 @@ def render_views(field, cams, n_threads: int = 0, images: bool = False):
         rgbu = np.zeros((V, H, W, 4), dtype=np.float32)
     if n_threads <= 0:
         n_threads = os.cpu_count() or 1
-    L.orc_render_views(_p(planes), field.n, field.sh_degree, _p(cams), V, n_threads, _p(rgbu),
-                       _p(scores), _p(nf), _p(nk))
+    ls, keep = _lod(lod)
+    L.orc_render_views(_p(planes), field.n, field.sh_degree, _p(cams), V, ctypes.byref(ls) if ls else None,
+                       n_threads, _p(rgbu), _p(scores), _p(nf), _p(nk))
     return scores, nf, nk, rgbu
 
 

@@ -38,6 +38,15 @@ typedef struct {
   int32_t width, height;
 } orc_camera;
 
+/* NEXT-2 LOD blending parameters (PAPER.md eq:lod_blend L124-127 and its
+   clamped form, App. A.4); tile_level [n][4] = (tile centre, level). */
+typedef struct {
+  int32_t levels;
+  float delta;
+  float thresholds[7];
+  const float* tile_level;
+} orc_lod;
+
 /* one projected (view, Gaussian) pair */
 typedef struct {
   float u, v, A, B, C, o, unc, r, g, b;
@@ -119,6 +128,25 @@ void orc_sh_basis(float x, float y, float z, float Y[16]) {
   Y[15] = (-SH_C3a * x) * (xx - (3.0f * yy));
 }
 
+/* eq:lod_blend, clamped (App. A.4): a(d, D) = max(0, min(1, 0.5 - (d - D) / (2 delta))).
+   Level i fades out around D_i; level i+1 fades in with the complement
+   (DESIGN.md reading, "the coarser level taking the complement");
+   the weight of a level is the smaller of its fade-in and fade-out. */
+float orc_lod_blend(float d, float D, float delta) {
+  float a = 0.5f - (d - D) / (2.0f * delta);
+  return fminf(1.0f, fmaxf(0.0f, a));
+}
+
+float orc_lod_weight(float d, int level, const orc_lod* lod) {
+  float w = 1.0f;
+  if (level < lod->levels - 1) w = orc_lod_blend(d, lod->thresholds[level], lod->delta);
+  if (level > 0) {
+    float fin = 1.0f - orc_lod_blend(d, lod->thresholds[level - 1], lod->delta);
+    w = fminf(w, fin);
+  }
+  return w;
+}
+
 /* O1 step 15: span [x0, x1) of tile columns of tile row ty.  The pixel rows
    of the tile inside [py0, py1] form the band [ya, yb]; over the band the
    ellipse q <= t, whose x-interval at offset dy is
@@ -146,12 +174,25 @@ void orc_row_span(const orc_proj* p, uint32_t ty, int W, uint32_t* x0, uint32_t*
 /* planes: float32 [P][n][4]; plane 0 (x,y,z,o), 1 (sx,sy,sz,unc), 2 (qw,qx,qy,qz),
    3.. SH slot-major.  Projects Gaussian g into camera cam. */
 void orc_project_one(const float* planes, int64_t n, int sh_degree, const orc_camera* cam,
-                     int64_t g, orc_proj* out) {
+                     const orc_lod* lod, int64_t g, orc_proj* out) {
   memset(out, 0, sizeof(*out));
   const float* po = planes + 4 * g;
   const float* su = planes + 4 * (n + g);
   const float* qq = planes + 4 * (2 * n + g);
-  const float mx = po[0], my = po[1], mz = po[2], o = po[3];
+  const float mx = po[0], my = po[1], mz = po[2];
+  float o = po[3];
+  /* NEXT-2: LOD blending scales the opacity by w at camera distance d from the
+     Gaussian's tile centre; o w < 1/255 can never reach alpha >= 1/255: cull. */
+  if (lod) {
+    const float* tl = lod->tile_level + 4 * g;
+    int level = (int)tl[3];
+    if (level < 0) level = 0;
+    if (level > lod->levels - 1) level = lod->levels - 1;
+    float ddx = cam->campos[0] - tl[0], ddy = cam->campos[1] - tl[1], ddz = cam->campos[2] - tl[2];
+    float d = sqrtf((ddx * ddx + ddy * ddy) + ddz * ddz);
+    o = o * orc_lod_weight(d, level, lod);
+    if (!(o >= ORC_ALPHA_MIN)) return;
+  }
   const float* R = cam->R;
   /* 1. view transform */
   float vx = ((R[0] * mx + R[1] * my) + R[2] * mz) + cam->t[0];
@@ -262,8 +303,9 @@ void orc_project_one(const float* planes, int64_t n, int sh_degree, const orc_ca
   out->r = rgb[0]; out->g = rgb[1]; out->b = rgb[2];
 }
 
-void orc_project(const float* planes, int64_t n, int sh_degree, const orc_camera* cam, orc_proj* out) {
-  for (int64_t g = 0; g < n; ++g) orc_project_one(planes, n, sh_degree, cam, g, &out[g]);
+void orc_project(const float* planes, int64_t n, int sh_degree, const orc_camera* cam, const orc_lod* lod,
+                 orc_proj* out) {
+  for (int64_t g = 0; g < n; ++g) orc_project_one(planes, n, sh_degree, cam, lod, g, &out[g]);
 }
 
 /* O2: number of keys of one view */
@@ -431,6 +473,7 @@ double orc_composite_brute(const orc_proj* p, int64_t n, const orc_camera* cam, 
 typedef struct {
   const float* planes; int64_t n; int sh_degree;
   const orc_camera* cams; int32_t n_views;
+  const orc_lod* lod;   /* opt */
   float* rgbu;          /* opt [V][H][W][4] */
   double* scores;       /* [V] */
   uint64_t* n_frag;     /* [V] */
@@ -442,7 +485,7 @@ static void render_one(orc_job* J, int v) {
   const orc_camera* cam = &J->cams[v];
   int64_t n = J->n;
   orc_proj* p = (orc_proj*)malloc(sizeof(orc_proj) * (size_t)(n > 0 ? n : 1));
-  orc_project(J->planes, n, J->sh_degree, cam, p);
+  orc_project(J->planes, n, J->sh_degree, cam, J->lod, p);
   int64_t k = orc_count_keys(p, n);
   uint64_t* keys = (uint64_t*)malloc(sizeof(uint64_t) * (size_t)(k > 0 ? k : 1));
   uint32_t* vals = (uint32_t*)malloc(sizeof(uint32_t) * (size_t)(k > 0 ? k : 1));
@@ -477,10 +520,10 @@ static void* worker(void* arg) {
 /* Render and score n_views views (same W,H when rgbu is given) on n_threads
    host threads, one view per thread at a time. */
 void orc_render_views(const float* planes, int64_t n, int sh_degree, const orc_camera* cams,
-                      int32_t n_views, int n_threads, float* rgbu, double* scores, uint64_t* n_frag,
-                      int64_t* n_keys) {
+                      int32_t n_views, const orc_lod* lod, int n_threads, float* rgbu, double* scores,
+                      uint64_t* n_frag, int64_t* n_keys) {
   orc_job J;
-  J.planes = planes; J.n = n; J.sh_degree = sh_degree; J.cams = cams; J.n_views = n_views;
+  J.planes = planes; J.n = n; J.sh_degree = sh_degree; J.cams = cams; J.n_views = n_views; J.lod = lod;
   J.rgbu = rgbu; J.scores = scores; J.n_frag = n_frag; J.n_keys = n_keys; J.next = 0;
   pthread_mutex_init(&J.mu, NULL);
   if (n_threads < 1) n_threads = 1;

@@ -7,6 +7,6 @@ views, ``distributed`` shards views across GPUs.  No CPU fallback: importing
 this package without a built libgsr.so raises ImportError.
 """
 from . import gsr  # noqa: F401  (loads libgsr.so or fails loudly)
-from .gsr import CAM_DTYPE, Context, Gaussians, GsrError  # noqa: F401
+from .gsr import CAM_DTYPE, Context, Gaussians, GsrError, Lod  # noqa: F401
 
-__all__ = ["gsr", "CAM_DTYPE", "Context", "Gaussians", "GsrError"]
+__all__ = ["gsr", "CAM_DTYPE", "Context", "Gaussians", "GsrError", "Lod"]

@@ -189,7 +189,7 @@ gsr_status gsr_camera_look_at(double elevation, double azimuth, double radius, c
 }
 
 gsr_status gsr_project(gsr_ctx* ctx, const gsr_gaussians* G, const gsr_camera* cams, int32_t n_views,
-                       float* render_rec, uint32_t* bin_rec, void* stream) {
+                       const gsr_lod* lod, float* render_rec, uint32_t* bin_rec, void* stream) {
   if (!ctx) return GSR_EINVAL;
   if (!G || !cams || !render_rec || !bin_rec) return set_err(ctx, GSR_EINVAL, "gsr_project: NULL required pointer");
   if (G->n < 0 || G->sh_degree < 0 || G->sh_degree > 3)
@@ -207,6 +207,20 @@ gsr_status gsr_project(gsr_ctx* ctx, const gsr_gaussians* G, const gsr_camera* c
   if (tiles * (uint64_t)n_views >= (1ull << 32)) return set_err(ctx, GSR_EINVAL, "gsr_project: V*tiles >= 2^32");
   if (W > 65535 || H > 65535)
     return set_err(ctx, GSR_EINVAL, "gsr_project: W or H > 65535 (16-bit pixel-row fields of the span record)");
+  LodParams lp;
+  std::memset(&lp, 0, sizeof(lp));
+  if (lod) {
+    if (lod->levels < 1 || lod->levels > 8 || !(lod->delta > 0.0f) || (G->n > 0 && !lod->tile_level))
+      return set_err(ctx, GSR_EINVAL, "gsr_project: bad LOD (levels in [1,8], delta > 0, tile_level required)");
+    for (int i = 1; i + 1 < lod->levels; ++i)
+      if (!(lod->thresholds[i] > lod->thresholds[i - 1]))
+        return set_err(ctx, GSR_EINVAL, "gsr_project: LOD thresholds must increase");
+    lp.on = 1;
+    lp.levels = lod->levels;
+    lp.delta = lod->delta;
+    for (int i = 0; i < 7; ++i) lp.D[i] = lod->thresholds[i];
+    lp.tile_level = lod->tile_level;
+  }
   if (G->n == 0) return GSR_OK;
   CamBatch cb;
   std::memset(&cb, 0, sizeof(cb));
@@ -217,7 +231,8 @@ gsr_status gsr_project(gsr_ctx* ctx, const gsr_gaussians* G, const gsr_camera* c
   const int planes = 3 + (3 * (G->sh_degree + 1) * (G->sh_degree + 1) + 3) / 4;
   account(ctx, GSR_STAGE_PROJECT, 1, 16.0 * planes * (double)G->n + 8.0 * n_views * (double)G->n);
   StageScope sc(ctx, GSR_STAGE_PROJECT, (cudaStream_t)stream);
-  return check_cuda(ctx, launch_project(*G, cb, n_views, render_rec, bin_rec, (cudaStream_t)stream), "k1_project");
+  if (lp.on) account(ctx, GSR_STAGE_PROJECT, 0, 16.0 * (double)G->n);
+  return check_cuda(ctx, launch_project(*G, cb, lp, n_views, render_rec, bin_rec, (cudaStream_t)stream), "k1_project");
 }
 
 }  // extern "C"

@@ -26,6 +26,13 @@ struct CamBatch {
   gsr_camera c[GSR_MAX_VIEWS];
 };
 
+struct LodParams {  // NEXT-2 LOD blending (gsr_lod), kernel parameter
+  int on, levels;
+  float delta;
+  float D[7];
+  const float* tile_level;
+};
+
 // exp(x) for x <= 0: Cody-Waite range reduction by ln2 (hi/lo), degree-7
 // Taylor polynomial in Horner form, scale by 2^k built in the exponent field.
 // Pure IEEE float ops -> bit-identical on any correctly rounding FPU.
@@ -140,7 +147,7 @@ struct StageScope {
 };
 
 // ---- launchers (each returns cudaGetLastError() of its launches) ----
-cudaError_t launch_project(const gsr_gaussians& G, const CamBatch& cams, int V, float* rec,
+cudaError_t launch_project(const gsr_gaussians& G, const CamBatch& cams, const LodParams& lod, int V, float* rec,
                            uint32_t* bin, cudaStream_t st);
 
 // onesweep radix sort pieces (binsort.cu)

@@ -74,6 +74,7 @@ __global__ void __launch_bounds__(256) k1_project(const float4* __restrict__ po,
                                                   const float4* __restrict__ rq, const float4* __restrict__ sh,
                                                   int64_t n, int V, int W, int H,
                                                   const __grid_constant__ CamBatch cams,
+                                                  const __grid_constant__ LodParams lod,
                                                   float4* __restrict__ rec, uint32_t* __restrict__ bin) {
   const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (g >= n) return;
@@ -86,7 +87,13 @@ __global__ void __launch_bounds__(256) k1_project(const float4* __restrict__ po,
     const float4 c = __ldg(sh + (int64_t)j * n + g);
     S.k[4 * j + 0] = c.x; S.k[4 * j + 1] = c.y; S.k[4 * j + 2] = c.z; S.k[4 * j + 3] = c.w;
   }
-  const float mx = P.x, my = P.y, mz = P.z, o = P.w;
+  const float mx = P.x, my = P.y, mz = P.z, o0 = P.w;
+  float4 TL = make_float4(0.f, 0.f, 0.f, 0.f);
+  int level = 0;
+  if (lod.on) {
+    TL = __ldg(reinterpret_cast<const float4*>(lod.tile_level) + g);
+    level = min(max((int)TL.w, 0), lod.levels - 1);
+  }
 
   // view-independent 3D covariance (O1 steps 4-7)
   const float qn = sqrtf(((Q4.x * Q4.x + Q4.y * Q4.y) + Q4.z * Q4.z) + Q4.w * Q4.w);
@@ -113,11 +120,12 @@ __global__ void __launch_bounds__(256) k1_project(const float4* __restrict__ po,
 #pragma unroll
     for (int j = 0; j < 3; ++j) Sg[i][j] = (M[i][0] * M[j][0] + M[i][1] * M[j][1]) + M[i][2] * M[j][2];
 
-  // alpha-skip bound (GPU-only shortcut, exact semantics): power < tau implies
-  // o * exp(power) < 1/255 with a 1e-3 margin far above exp_spec's 1.1e-7 error.
-  const float tau = -logf(255.0f * o) - 1e-3f;
-  const float thr = 2.0f * logf(255.0f * o) + 2e-3f;  // q threshold of the alpha >= 1/255 region
 
+  // alpha-skip bound (GPU-only shortcut, exact semantics): power < tau implies
+  // o * exp(power) < 1/255 with a 1e-3 margin far above exp_spec's 1.1e-7 error;
+  // thr = q bound of the alpha >= 1/255 region.  Per view under LOD blending.
+  const float tau0 = -logf(255.0f * o0) - 1e-3f;
+  const float thr0 = 2.0f * logf(255.0f * o0) + 2e-3f;
   const int64_t VN = (int64_t)V * n;
   uint4* span = reinterpret_cast<uint4*>(bin);        // [V*n][2] span records
   uint32_t* depth_plane = bin + 8 * VN;               // [V*n]
@@ -127,10 +135,23 @@ __global__ void __launch_bounds__(256) k1_project(const float4* __restrict__ po,
     const float* R = cam.R;
     const int64_t cg = (int64_t)c * n + g;
     uint32_t depth = 0, nt = 0;
+    // NEXT-2: LOD blend weight (eq:lod_blend, clamped form of App. A.4)
+    float o = o0;
+    bool lod_cull = false;
+    if (lod.on) {
+      const float ddx = cam.campos[0] - TL.x, ddy = cam.campos[1] - TL.y, ddz = cam.campos[2] - TL.z;
+      const float d = sqrtf((ddx * ddx + ddy * ddy) + ddz * ddz);
+      const float two_delta = 2.0f * lod.delta;
+      float w = 1.0f;
+      if (level < lod.levels - 1) w = fminf(1.0f, fmaxf(0.0f, 0.5f - (d - lod.D[level]) / two_delta));
+      if (level > 0) w = fminf(w, 1.0f - fminf(1.0f, fmaxf(0.0f, 0.5f - (d - lod.D[level - 1]) / two_delta)));
+      o = o0 * w;
+      lod_cull = !(o >= __uint_as_float(kAlphaMinBits));
+    }
     const float vx = ((R[0] * mx + R[1] * my) + R[2] * mz) + cam.t[0];
     const float vy = ((R[3] * mx + R[4] * my) + R[5] * mz) + cam.t[1];
     const float vz = ((R[6] * mx + R[7] * my) + R[8] * mz) + cam.t[2];
-    if (vz > cam.znear) {
+    if (vz > cam.znear && !lod_cull) {
       const float xn = vx / vz, yn = vy / vz;
       const float u = cam.fx * xn + cam.cx;
       const float v = cam.fy * yn + cam.cy;
@@ -173,6 +194,11 @@ __global__ void __launch_bounds__(256) k1_project(const float4* __restrict__ po,
           nt = ntt;
           span[2 * cg] = make_uint4(__float_as_uint(u), __float_as_uint(v), __float_as_uint(sp), __float_as_uint(sh));
           span[2 * cg + 1] = make_uint4(__float_as_uint(sic), __float_as_uint(sdys), py0 | (py1 << 16), ntt);
+          float tau = tau0, thr = thr0;
+          if (lod.on) {
+            tau = -logf(255.0f * o) - 1e-3f;
+            thr = 2.0f * logf(255.0f * o) + 2e-3f;
+          }
           const float inv = 1.0f / det;
           const float A = cc * inv, B = -(b * inv), C = a * inv;
           // SH colour
@@ -202,8 +228,8 @@ __global__ void __launch_bounds__(256) k1_project(const float4* __restrict__ po,
 
 }  // namespace
 
-cudaError_t launch_project(const gsr_gaussians& G, const CamBatch& cams, int V, float* rec, uint32_t* bin,
-                           cudaStream_t st) {
+cudaError_t launch_project(const gsr_gaussians& G, const CamBatch& cams, const LodParams& lod, int V, float* rec,
+                           uint32_t* bin, cudaStream_t st) {
   const int W = cams.c[0].width, H = cams.c[0].height;
   const int64_t n = G.n;
   const unsigned blocks = (unsigned)((n + 255) / 256);
@@ -213,10 +239,10 @@ cudaError_t launch_project(const gsr_gaussians& G, const CamBatch& cams, int V, 
   auto sh = reinterpret_cast<const float4*>(G.sh);
   auto r4 = reinterpret_cast<float4*>(rec);
   switch (G.sh_degree) {
-    case 0: k1_project<0><<<blocks, 256, 0, st>>>(po, su, rq, sh, n, V, W, H, cams, r4, bin); break;
-    case 1: k1_project<1><<<blocks, 256, 0, st>>>(po, su, rq, sh, n, V, W, H, cams, r4, bin); break;
-    case 2: k1_project<2><<<blocks, 256, 0, st>>>(po, su, rq, sh, n, V, W, H, cams, r4, bin); break;
-    default: k1_project<3><<<blocks, 256, 0, st>>>(po, su, rq, sh, n, V, W, H, cams, r4, bin); break;
+    case 0: k1_project<0><<<blocks, 256, 0, st>>>(po, su, rq, sh, n, V, W, H, cams, lod, r4, bin); break;
+    case 1: k1_project<1><<<blocks, 256, 0, st>>>(po, su, rq, sh, n, V, W, H, cams, lod, r4, bin); break;
+    case 2: k1_project<2><<<blocks, 256, 0, st>>>(po, su, rq, sh, n, V, W, H, cams, lod, r4, bin); break;
+    default: k1_project<3><<<blocks, 256, 0, st>>>(po, su, rq, sh, n, V, W, H, cams, lod, r4, bin); break;
   }
   return cudaGetLastError();
 }

@@ -49,6 +49,11 @@ class _Gaussians(ctypes.Structure):
                 ("sh", ctypes.c_void_p)]
 
 
+class _Lod(ctypes.Structure):
+    _fields_ = [("levels", ctypes.c_int32), ("delta", ctypes.c_float), ("thresholds", ctypes.c_float * 7),
+                ("tile_level", ctypes.c_void_p)]
+
+
 def _load():
     if not os.path.exists(LIB_PATH):
         raise ImportError(f"libgsr.so not built at {LIB_PATH}: run `python -c 'import __graft_entry__ as g; "
@@ -61,7 +66,7 @@ def _load():
     L.gsr_last_error.restype = ctypes.c_char_p
     L.gsr_version.restype = ctypes.c_char_p
     L.gsr_camera_look_at.argtypes = [ctypes.c_double] * 3 + [P, i32, i32, ctypes.c_double, ctypes.c_double, P]
-    L.gsr_project.argtypes = [P, P, P, i32, P, P, P]
+    L.gsr_project.argtypes = [P, P, P, i32, P, P, P, P]
     L.gsr_bin_sort.argtypes = [P, P, i64, P, i32, P, P, i64, P, P, P, P, P]
     L.gsr_composite.argtypes = [P, P, i64, P, P, P, i32, P, P, P, P, P, P, P]
     L.gsr_sobel_scores.argtypes = [P, P, P, i32, P, P, P]
@@ -137,6 +142,22 @@ class Gaussians:
         return _Gaussians(self.n, self.sh_degree, 0, base, base + stride, base + 2 * stride, base + 3 * stride)
 
 
+class Lod:
+    """NEXT-2 LOD blending (gsr_lod): device tile_level [n][4] float32 tensor
+    (tile centre x, y, z, level) + levels, bandwidth delta and thresholds."""
+
+    def __init__(self, tile_level, levels: int, delta: float, thresholds):
+        assert tile_level.is_cuda and tile_level.dtype.is_floating_point and tile_level.shape[-1] == 4
+        self.tile_level = tile_level.contiguous()
+        self.levels = int(levels)
+        self.delta = float(delta)
+        self.thresholds = [float(x) for x in thresholds]
+
+    def struct(self) -> _Lod:
+        th = (ctypes.c_float * 7)(*(self.thresholds + [0.0] * (7 - len(self.thresholds))))
+        return _Lod(self.levels, self.delta, th, self.tile_level.data_ptr())
+
+
 class Context:
     """A gsr_ctx (scratch owner) bound to one device; one per stream/thread."""
 
@@ -178,11 +199,13 @@ class Context:
         return {s: dict(ms=float(ms[i]), launches=int(la[i]), bytes=float(by[i])) for i, s in enumerate(STAGES)}
 
 
-def gsr_project(ctx: Context, g: Gaussians, cams, render_rec, bin_rec, stream=None):
+def gsr_project(ctx: Context, g: Gaussians, cams, render_rec, bin_rec, stream=None, lod: Optional[Lod] = None):
     c = cams_array(cams)
     gs = g.struct()
-    ctx._check(lib.gsr_project(ctx.handle, ctypes.byref(gs), c.ctypes.data, len(c), _ptr(render_rec),
-                               _ptr(bin_rec), _stream(stream)))
+    ls = lod.struct() if lod is not None else None
+    ctx._check(lib.gsr_project(ctx.handle, ctypes.byref(gs), c.ctypes.data, len(c),
+                               ctypes.byref(ls) if ls is not None else None, _ptr(render_rec), _ptr(bin_rec),
+                               _stream(stream)))
 
 
 def gsr_bin_sort(ctx: Context, bin_rec, n: int, cams, vals, capacity: int, ranges, keys=None,

@@ -65,8 +65,9 @@ class ViewScorer:
     capacity follows gsr_bin_sort's capacity protocol (GSR_ECAPACITY returns
     the required size; grow by 25 % and retry)."""
 
-    def __init__(self, field: Gaussians, batch_views: int = 16, n_slots: int = 2):
+    def __init__(self, field: Gaussians, batch_views: int = 16, n_slots: int = 2, lod: Optional[gsr.Lod] = None):
         self.field = field
+        self.lod = lod  # NEXT-2 LOD blending (opacity multiplier in K1), or None
         self.dev = field.planes.device
         self.V = min(int(batch_views), gsr.GSR_MAX_VIEWS)
         self.slots: List[_Slot] = []
@@ -164,7 +165,7 @@ class ViewScorer:
             st.wait_stream(S.comp)  # the previous composite of this slot still reads rec / vals / ranges
         # rec / bin hold [V][n][12] and [10 V n] for THIS batch's V, packed from the
         # start of the (batch_views-sized) buffers: the base pointers are passed.
-        gsr.gsr_project(S.ctx, self.field, cams, S.rec, S.bin, st)
+        gsr.gsr_project(S.ctx, self.field, cams, S.rec, S.bin, st, lod=self.lod)
         while True:
             try:
                 K = gsr.gsr_bin_sort(S.ctx, S.bin, n, cams, S.vals, S.capacity, S.ranges,

@@ -2,7 +2,7 @@
 # A/B of K6 / pipeline variants on the bench workload (GPU box), then one
 # ncu --set full capture of K6 with source.  Outputs under gpurun_out/.
 mkdir -p gpurun_out
-B="python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-e2e"
+B="python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-e2e --no-extras"
 for cfg in "base:" "slots1:--slots 1" "pix2:GSR_PIX=2" "stages8:GSR_STAGES=8" "pix2s8:GSR_PIX=2 GSR_STAGES=8"; do
   name=${cfg%%:*}; rest=${cfg#*:}
   envs=""; args=""

@@ -4,7 +4,7 @@
 #    on the top kernels.  Outputs under gpurun_out/.
 TAG=${1:-r1}
 KRE=${2:-"k6_composite|onesweep|k3_emit"}
-CMD="python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e --slots ${SLOTS:-1}"
+CMD="python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e --no-extras --slots ${SLOTS:-1}"
 mkdir -p gpurun_out
 $CMD > gpurun_out/plain_$TAG.log 2>&1 || { echo "plain run failed"; tail -20 gpurun_out/plain_$TAG.log; exit 1; }
 ncu --metrics gpu__time_duration.sum --clock-control none -s 300 -c 400 --csv \

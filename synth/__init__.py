@@ -224,7 +224,7 @@ def gen_config1_field(n: int = 10_000, seed: int = 0) -> GaussianField:
 
 
 def gen_terrain_field(n: int, seed: int, lo: float, hi: float, sh_degree: int = 3,
-                      offset=(0.0, 0.0, 0.0)) -> GaussianField:
+                      offset=(0.0, 0.0, 0.0), logscale_mu: float = -4.5) -> GaussianField:
     """configs[1..4]: x,z ~ U[lo,hi]; y = 0.1 sin(3x) cos(3z) + N(0,0.02);
     log s ~ N(-4.5,0.6); o = sigmoid(N(0.5,1)); SH DC ~ U[0,1], rest N(0,0.05);
     u ~ Beta(2,5).  ``offset`` translates (config 4 tile placement)."""
@@ -234,7 +234,7 @@ def gen_terrain_field(n: int, seed: int, lo: float, hi: float, sh_degree: int = 
     x, z = xz[:, 0], xz[:, 1]
     y = 0.1 * np.sin(3.0 * x) * np.cos(3.0 * z) + noise
     means = np.stack([x, y, z], axis=1) + np.asarray(offset, dtype=np.float64)
-    scales, q, opac = _activate(rng, n, -4.5, 0.6, 0.5, means)
+    scales, q, opac = _activate(rng, n, logscale_mu, 0.6, 0.5, means)
     ncoef = (sh_degree + 1) ** 2
     sh = np.zeros((n, ncoef, 3))
     sh[:, 0, :] = rng.uniform(0.0, 1.0, size=(n, 3))
@@ -285,6 +285,70 @@ def gen_config4_field(n_per_tile: int = 500_000) -> GaussianField:
             # each distinct tile is the same draw (seed 1000+t) placed at (i, 0, j)
             parts.append(gen_terrain_field(n_per_tile, 1000 + t, 0.0, 1.0, 3, offset=(i, 0.0, j)))
     return concat_fields(parts)
+
+
+# --------------------------------------------------------------------------
+# NEXT-2 LOD data (§3.5 eq:lod_blend; tab:dav-gswt-lod L205-246)
+# --------------------------------------------------------------------------
+@dataclass
+class LodData:
+    """Per-Gaussian (tile centre x, y, z, level) + the blend parameters."""
+    tile_level: np.ndarray  # float32 [n][4]
+    levels: int
+    delta: float
+    thresholds: tuple
+
+
+# Readings (DESIGN.md): six levels (§4.4), thresholds doubling from 1.5 tile
+# widths, bandwidth 0.25 (2 delta < every threshold gap, SPEC S:L548); each
+# coarser level has 1/4 of the Gaussians (tab:dav-gswt-lod: 3.7-3.9x per level)
+# and 2.3x the scale (0.0032 -> 0.20 over five levels in the same table).
+LOD_LEVELS = 6
+LOD_THRESHOLDS = (1.5, 3.0, 6.0, 12.0, 24.0)
+LOD_DELTA = 0.25
+LOD_COUNT_STEP = 4
+LOD_SCALE_STEP = 2.3
+
+
+def gen_lod_tile(n0: int, seed: int, offset=(0.0, 0.0, 0.0), levels: int = LOD_LEVELS):
+    """One unit-square terrain tile with ``levels`` LOD levels drawn as in
+    configs[1] (level l: n0 / 4^l Gaussians, log-scale mean -4.5 + l ln 2.3,
+    seed 16 seed + l).  Returns (field, tile_level [n][4])."""
+    parts, tl = [], []
+    centre = (offset[0] + 0.5, offset[1], offset[2] + 0.5)
+    for l in range(levels):
+        nl = max(1, n0 // LOD_COUNT_STEP ** l)
+        parts.append(gen_terrain_field(nl, 16 * seed + l, 0.0, 1.0, 3, offset,
+                                       logscale_mu=-4.5 + l * math.log(LOD_SCALE_STEP)))
+        t = np.zeros((nl, 4), dtype=np.float32)
+        t[:, 0:3] = centre
+        t[:, 3] = l
+        tl.append(t)
+    return concat_fields(parts), np.concatenate(tl)
+
+
+def gen_config4_lod(n_per_tile: int = 500_000):
+    """configs[3] with NEXT-2 LOD levels: the 4x4 Wang assembly of 8 distinct
+    tiles, each tile carrying six levels; returns (field, LodData)."""
+    assign = wang_assignment()
+    fields, tls = [], []
+    for j in range(4):
+        for i in range(4):
+            t = int(assign[j, i])
+            f, tl = gen_lod_tile(n_per_tile, 1000 + t, offset=(i, 0.0, j))
+            fields.append(f)
+            tls.append(tl)
+    return concat_fields(fields), LodData(np.ascontiguousarray(np.concatenate(tls)), LOD_LEVELS, LOD_DELTA,
+                                          LOD_THRESHOLDS)
+
+
+def random_lod(rng, n: int, levels: int = 4, thresholds=(1.0, 2.0, 3.0), delta: float = 0.3,
+               centre_range: float = 1.5) -> LodData:
+    """Random tile centres and levels for parity tests."""
+    tl = np.zeros((n, 4), dtype=np.float32)
+    tl[:, 0:3] = rng.uniform(-centre_range, centre_range, size=(n, 3))
+    tl[:, 3] = rng.integers(0, levels, size=n)
+    return LodData(tl, levels, delta, tuple(thresholds))
 
 
 # --------------------------------------------------------------------------

@@ -10,7 +10,14 @@ def to_dev(field):
     return Gaussians(torch.from_numpy(np.ascontiguousarray(field.planes)).cuda(), field.sh_degree)
 
 
-def gpu_batch(ctx, field, cams, images=True, want_unsorted=True, want_keys=True, want_gray=False):
+def to_dev_lod(lod):
+    from paper_2602_15355_b200 import Lod
+    if lod is None:
+        return None
+    return Lod(torch.from_numpy(np.ascontiguousarray(lod.tile_level)).cuda(), lod.levels, lod.delta, lod.thresholds)
+
+
+def gpu_batch(ctx, field, cams, images=True, want_unsorted=True, want_keys=True, want_gray=False, lod=None):
     """One batch (len(cams) <= 64, same W,H) through K1..K7; numpy outputs."""
     from paper_2602_15355_b200 import gsr
     G = to_dev(field)
@@ -20,7 +27,7 @@ def gpu_batch(ctx, field, cams, images=True, want_unsorted=True, want_keys=True,
     T = V * gx * gy
     rec = torch.full((V, max(n, 1), 12), float("nan"), dtype=torch.float32, device="cuda")
     binr = torch.full((10 * V * max(n, 1),), -1, dtype=torch.int32, device="cuda")
-    gsr.gsr_project(ctx, G, cams, rec, binr)
+    gsr.gsr_project(ctx, G, cams, rec, binr, lod=to_dev_lod(lod))
     cap = 0
     vals = torch.empty(1, dtype=torch.int32, device="cuda")
     ranges = torch.full((T, 2), -1, dtype=torch.int32, device="cuda")
@@ -67,9 +74,9 @@ def gpu_batch(ctx, field, cams, images=True, want_unsorted=True, want_keys=True,
     return out
 
 
-def oracle_batch(field, cams, images=True):
+def oracle_batch(field, cams, images=True, lod=None):
     """The oracle's expected outputs for the same batch."""
-    projs = [oracle.project(field, c) for c in cams]
+    projs = [oracle.project(field, c, lod) for c in cams]
     bs = oracle.bin_sort_batch(projs, cams)
     gx, gy = oracle.grid(cams[0])
     tpv = gx * gy

@@ -27,9 +27,9 @@ def ctx():
     return Context(0)
 
 
-def _full_check(ctx, field, cams, images=True):
-    g = gpu_batch(ctx, field, cams, images=images)
-    o = oracle_batch(field, cams, images=images)
+def _full_check(ctx, field, cams, images=True, lod=None):
+    g = gpu_batch(ctx, field, cams, images=images, lod=lod)
+    o = oracle_batch(field, cams, images=images, lod=lod)
     check_projection(g, o, field.n)
     assert g["K"] == len(o["keys"])
     assert np.array_equal(g["keys_unsorted"], o["keys_unsorted"]), "unsorted keys"
