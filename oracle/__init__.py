@@ -91,6 +91,8 @@ def lib():
         L.orc_composite_tiled.restype = ctypes.c_double
         L.orc_composite_brute.argtypes = [P, i64, P, P, P, P, P]
         L.orc_composite_brute.restype = ctypes.c_double
+        L.orc_composite_trace.argtypes = [P, P, P, P, P, P, i64]
+        L.orc_composite_trace.restype = i64
         L.orc_render_views.argtypes = [P, i64, ctypes.c_int, P, i32, P, ctypes.c_int, P, P, P, P]
         _lib = L
     return _lib
@@ -235,6 +237,22 @@ def composite_tiled(proj, sorted_vals, ranges_view, cam):
     score = L.orc_composite_tiled(_p(proj), _p(sv if len(sv) else np.zeros(1, np.uint32)), _p(rv),
                                   _p(c), _p(rgbu), _p(tf), _p(nc), _p(nf))
     return dict(rgbu=rgbu, t_final=tf, n_contrib=nc, score=score, n_frag=int(nf[0]), n_eval=int(nf[1]))
+
+
+def composite_trace(proj, sorted_vals, ranges_view, cam):
+    """NEXT-3: per pixel (row-major), the Gaussians the O5 loop blends, in
+    order -> (offsets int64 [H*W+1], idx uint32 [total])."""
+    L = lib()
+    c = _cam(cam)
+    W, H = _wh(c)
+    off = np.zeros(W * H + 1, dtype=np.int64)
+    sv = np.ascontiguousarray(sorted_vals, dtype=np.uint32)
+    rv = np.ascontiguousarray(ranges_view, dtype=np.uint32)
+    svp = _p(sv if len(sv) else np.zeros(1, np.uint32))
+    k = L.orc_composite_trace(_p(proj), svp, _p(rv), _p(c), _p(off), None, 0)
+    idx = np.zeros(max(k, 1), dtype=np.uint32)
+    L.orc_composite_trace(_p(proj), svp, _p(rv), _p(c), _p(off), _p(idx), k)
+    return off, idx[:k]
 
 
 def composite_brute(proj, cam):

@@ -427,6 +427,42 @@ double orc_composite_tiled(const orc_proj* p, const uint32_t* sorted_vals, const
   return sum / ((double)W * (double)H);
 }
 
+/* NEXT-3 support: the blended entries of every pixel of one view, in
+   compositing order (the same O5 loop as composite_pixel, recording g
+   instead of accumulating).  offsets [H*W+1] (pixel row-major); idx [cap]
+   receives the Gaussian indices.  Returns the total count (idx is filled up
+   to cap).  The float32 decisions (skip, stop) are exactly the forward's. */
+int64_t orc_composite_trace(const orc_proj* p, const uint32_t* sorted_vals, const uint32_t* ranges_view,
+                            const orc_camera* cam, int64_t* offsets, uint32_t* idx, int64_t cap) {
+  int W = cam->width, H = cam->height;
+  int gx = (W + ORC_TILE - 1) / ORC_TILE;
+  int64_t k = 0;
+  for (int py = 0; py < H; ++py)
+    for (int px = 0; px < W; ++px) {
+      offsets[(size_t)py * W + px] = k;
+      int tile = (py / ORC_TILE) * gx + (px / ORC_TILE);
+      uint32_t s = ranges_view[2 * tile], e = ranges_view[2 * tile + 1];
+      float pcx = (float)px + 0.5f, pcy = (float)py + 0.5f;
+      float T = 1.0f;
+      for (uint32_t i = s; i < e; ++i) {
+        const orc_proj* q = &p[sorted_vals[i]];
+        float dx = q->u - pcx, dy = q->v - pcy;
+        float qf = fmaf(q->A * dx, dx, (q->C * dy) * dy);
+        float power = fmaf(-0.5f, qf, -((q->B * dx) * dy));
+        if (power > 0.0f) continue;
+        float alpha = fminf(ORC_ALPHA_MAX, q->o * orc_exp_spec(power));
+        if (alpha < ORC_ALPHA_MIN) continue;
+        float tT = T * (1.0f - alpha);
+        if (tT < ORC_T_STOP) break;
+        if (k < cap) idx[k] = sorted_vals[i];
+        ++k;
+        T = tT;
+      }
+    }
+  offsets[(size_t)W * H] = k;
+  return k;
+}
+
 /* depth-then-index comparator for the brute-force list */
 static const orc_proj* g_brute_p;
 static int cmp_depth_index(const void* a, const void* b) {
