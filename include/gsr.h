@@ -224,6 +224,26 @@ gsr_status gsr_select_nbv(gsr_ctx* ctx, const float* scores, int32_t n, const ui
 gsr_status gsr_sobel_scores(gsr_ctx* ctx, const float* gray, const gsr_camera* cams, int32_t n_views,
                             float* tile_partial, float* scores, void* stream);
 
+/* ---- NEXT-3: backward rasterizer (UPDATE_GS, Alg. 1) --------
+   Vector-Jacobian product of the batch's composited images: with the
+   upstream gradient G = dL/d(r, g, b, U) per pixel, ADDS to `grads` the
+   gradient of L = sum_v sum_p <G_v(p), C_v(p)> w.r.t. every Gaussian
+   parameter, in the field's plane layout:
+     plane 0 (d mean xyz, d opacity), plane 1 (d scale xyz, d uncertainty),
+     plane 2 (d raw quaternion wxyz, through the normalisation), planes 3..
+     (d SH coefficients, flat index 3*coef + channel).
+   The blended (pixel, Gaussian) pairs and their order are the forward's (same
+   float32 decisions); the image is differentiated between those decisions
+   (alpha clamp, FOV clamp and max(0, colour) pass gradient only where
+   inactive).  Inputs are the forward products of THIS batch: render_rec /
+   bin_rec (gsr_project, same lod), vals / ranges (gsr_bin_sort), rgbu (the
+   forward image, gsr_composite), dl_drgbu [V][H][W][4].  Float atomics: the
+   sums are not bit-deterministic.  grads [P][n][4] float (device). */
+gsr_status gsr_backward(gsr_ctx* ctx, const gsr_gaussians* gaussians, const gsr_camera* cams, int32_t n_views,
+                        const gsr_lod* lod, const float* render_rec, const uint32_t* bin_rec,
+                        const uint32_t* vals, const uint32_t* ranges, const float* rgbu,
+                        const float* dl_drgbu, float* grads, void* stream);
+
 /* ---- NEXT-1: latent-space ensemble disagreement (PAPER.md eq:w2_pixel,
    §3.3) ---------------------------------------------------------------
    For each candidate view v: W2 = (1/(H_z W_z)) sum_p (1/C(M,2)) sum_{i<j}
@@ -264,7 +284,8 @@ enum {
   GSR_STAGE_SORT_U64 = 9,   /* utility sort (histogram + passes) */
   GSR_STAGE_W2 = 10,        /* NEXT-1 latent W2 scorer */
   GSR_STAGE_SOBEL = 11,     /* NEXT-4 Sobel image term */
-  GSR_N_STAGES = 12
+  GSR_STAGE_BACKWARD = 12,  /* NEXT-3 backward rasterizer (K6b + K1b) */
+  GSR_N_STAGES = 13
 };
 /* enable != 0: bracket every stage with CUDA events on its launch stream. */
 gsr_status gsr_timing_enable(gsr_ctx* ctx, int enable);

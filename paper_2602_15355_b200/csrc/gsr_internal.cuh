@@ -95,6 +95,7 @@ enum Slot {
   S_SORTK, S_SORTV,                         // utility sort ping-pong
   S_SELECT,                                 // exclusion mask staging
   S_SELECT2,                                // NEXT-1 per-chunk partial sums
+  S_GRAD2D,                                 // NEXT-3 per-(view, g) 2D gradients
   S_NSLOTS
 };
 

@@ -32,9 +32,9 @@ assert CAM_DTYPE.itemsize == 96
 EXPORTED = ["gsr_create", "gsr_destroy", "gsr_last_error", "gsr_version", "gsr_camera_look_at",
             "gsr_project", "gsr_bin_sort", "gsr_composite", "gsr_score_views", "gsr_select_nbv",
             "gsr_sort_pairs_u64", "gsr_scratch_bytes", "gsr_timing_enable", "gsr_timing_read", "gsr_w2_scores",
-            "gsr_sobel_scores"]
+            "gsr_sobel_scores", "gsr_backward"]
 STAGES = ["project", "compact", "depth_sort", "emit", "ranges", "tile_sort", "composite", "score", "select",
-          "sort_u64", "w2", "sobel"]
+          "sort_u64", "w2", "sobel", "backward"]
 
 
 class GsrError(RuntimeError):
@@ -70,6 +70,7 @@ def _load():
     L.gsr_bin_sort.argtypes = [P, P, i64, P, i32, P, P, i64, P, P, P, P, P]
     L.gsr_composite.argtypes = [P, P, i64, P, P, P, i32, P, P, P, P, P, P, P]
     L.gsr_sobel_scores.argtypes = [P, P, P, i32, P, P, P]
+    L.gsr_backward.argtypes = [P, P, P, i32, P, P, P, P, P, P, P, P, P]
     L.gsr_score_views.argtypes = [P, P, P, i32, P, P]
     L.gsr_select_nbv.argtypes = [P, P, i32, P, i32, P, P]
     L.gsr_sort_pairs_u64.argtypes = [P, P, P, P, P, i64, i32, i32, P]
@@ -230,6 +231,18 @@ def gsr_composite(ctx: Context, render_rec, n: int, vals, ranges, cams, tile_par
     ctx._check(lib.gsr_composite(ctx.handle, _ptr(render_rec), n, _ptr(vals), _ptr(ranges), c.ctypes.data, len(c),
                                  _ptr(rgbu), _ptr(t_final), _ptr(n_contrib), _ptr(gray), _ptr(tile_partial),
                                  _ptr(n_frag), _stream(stream)))
+
+
+def gsr_backward(ctx: Context, g: Gaussians, cams, render_rec, bin_rec, vals, ranges, rgbu, dl_drgbu, grads,
+                 lod: Optional["Lod"] = None, stream=None):
+    """NEXT-3: ADD dL/dparams ([P][n][4], the field's plane layout) for the
+    upstream image gradient dl_drgbu [V][H][W][4] of this batch's forward."""
+    c = cams_array(cams)
+    gs = g.struct()
+    ls = lod.struct() if lod is not None else None
+    ctx._check(lib.gsr_backward(ctx.handle, ctypes.byref(gs), c.ctypes.data, len(c),
+                                ctypes.byref(ls) if ls is not None else None, _ptr(render_rec), _ptr(bin_rec),
+                                _ptr(vals), _ptr(ranges), _ptr(rgbu), _ptr(dl_drgbu), _ptr(grads), _stream(stream)))
 
 
 def gsr_sobel_scores(ctx: Context, gray, cams, tile_partial, scores, stream=None):

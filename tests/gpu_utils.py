@@ -113,3 +113,33 @@ def check_projection(gpu, orc, n):
         for col, name in [(0, "u"), (1, "v"), (2, "A"), (3, "B"), (4, "C"), (5, "o"), (6, "unc"),
                           (8, "r"), (9, "g"), (10, "b")]:
             assert np.array_equal(r[:, col].view(np.uint32), p[name][vis].view(np.uint32)), f"view {v}: {name}"
+
+
+def gpu_forward_backward(ctx, field, cams, G, lod=None):
+    """Forward (K1..K6 with images) + NEXT-3 backward of one batch through the
+    C ABI; G [V][H][W][4] upstream gradient -> (rgbu, grads [P][n][4])."""
+    from paper_2602_15355_b200 import gsr
+    Gd = to_dev(field)
+    L = to_dev_lod(lod)
+    V, n = len(cams), field.n
+    W, H = int(cams[0]["width"]), int(cams[0]["height"])
+    T = V * ((W + 15) // 16) * ((H + 15) // 16)
+    rec = torch.zeros((V, max(n, 1), 12), dtype=torch.float32, device="cuda")
+    binr = torch.zeros((10 * V * max(n, 1),), dtype=torch.int32, device="cuda")
+    gsr.gsr_project(ctx, Gd, cams, rec, binr, lod=L)
+    ranges = torch.zeros((T, 2), dtype=torch.int32, device="cuda")
+    vals = torch.zeros(1, dtype=torch.int32, device="cuda")
+    try:
+        K = gsr.gsr_bin_sort(ctx, binr, n, cams, vals, 0, ranges)
+    except gsr.GsrError as e:
+        K = e.required
+    vals = torch.zeros(max(K, 1), dtype=torch.int32, device="cuda")
+    gsr.gsr_bin_sort(ctx, binr, n, cams, vals, max(K, 1), ranges)
+    partial = torch.zeros(T, dtype=torch.float32, device="cuda")
+    rgbu = torch.zeros((V, H, W, 4), dtype=torch.float32, device="cuda")
+    gsr.gsr_composite(ctx, rec, n, vals, ranges, cams, partial, rgbu=rgbu)
+    dG = torch.from_numpy(np.ascontiguousarray(G, dtype=np.float32)).cuda()
+    grads = torch.zeros_like(Gd.planes)
+    gsr.gsr_backward(ctx, Gd, cams, rec, binr, vals, ranges, rgbu, dG, grads, lod=L)
+    torch.cuda.synchronize()
+    return rgbu.cpu().numpy(), grads.cpu().numpy()
