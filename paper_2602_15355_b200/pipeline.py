@@ -218,3 +218,53 @@ class ViewScorer:
         out = torch.empty(k, dtype=torch.int32, device=self.dev)
         gsr.gsr_select_nbv(self.ctx, scores, k, out, exclude, torch.cuda.current_stream(self.dev))
         return out
+
+
+class Renderer:
+    """Forward images + NEXT-3 backward for one batch of views -- the
+    building block of UPDATE_GS (Alg. 1): ``forward(cams)``
+    renders (r, g, b, U) images and keeps the batch's products;
+    ``backward(dl_drgbu)`` adds dL/dparams (field plane layout) for an
+    upstream image gradient.  All arithmetic is in libgsr's kernels."""
+
+    def __init__(self, field: Gaussians, lod: Optional[gsr.Lod] = None):
+        self.field = field
+        self.lod = lod
+        self.ctx = Context(field.planes.device.index or 0)
+        self.dev = field.planes.device
+        self._cams = None
+
+    def forward(self, cams, stream=None) -> torch.Tensor:
+        cams = gsr.cams_array(cams)
+        V, n = len(cams), self.field.n
+        W, H = int(cams[0]["width"]), int(cams[0]["height"])
+        T = V * tiles_per_view(cams[0])
+        self.rec = torch.empty((V, max(n, 1), 12), dtype=torch.float32, device=self.dev)
+        self.bin = torch.empty(10 * V * max(n, 1), dtype=torch.int32, device=self.dev)
+        self.ranges = torch.empty((T, 2), dtype=torch.int32, device=self.dev)
+        gsr.gsr_project(self.ctx, self.field, cams, self.rec, self.bin, stream, lod=self.lod)
+        cap = getattr(self, "_cap", 1 << 20)
+        while True:
+            self.vals = torch.empty(cap, dtype=torch.int32, device=self.dev)
+            try:
+                gsr.gsr_bin_sort(self.ctx, self.bin, n, cams, self.vals, cap, self.ranges, stream=stream)
+                break
+            except GsrError as e:
+                if e.status != gsr.GSR_ECAPACITY:
+                    raise
+                cap = int(math.ceil(e.required * 1.25)) + 1024
+        self._cap = cap
+        self.partial = torch.empty(T, dtype=torch.float32, device=self.dev)
+        self.rgbu = torch.empty((V, H, W, 4), dtype=torch.float32, device=self.dev)
+        gsr.gsr_composite(self.ctx, self.rec, n, self.vals, self.ranges, cams, self.partial, rgbu=self.rgbu,
+                          stream=stream)
+        self._cams = cams
+        return self.rgbu
+
+    def backward(self, dl_drgbu: torch.Tensor, grads: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+        assert self._cams is not None, "forward() first"
+        if grads is None:
+            grads = torch.zeros_like(self.field.planes)
+        gsr.gsr_backward(self.ctx, self.field, self._cams, self.rec, self.bin, self.vals, self.ranges, self.rgbu,
+                         dl_drgbu.contiguous(), grads, lod=self.lod, stream=stream)
+        return grads

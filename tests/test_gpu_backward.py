@@ -61,3 +61,20 @@ def test_backward_is_linear_and_zero_for_zero_upstream(ctx):
     _, g0 = gpu_forward_backward(ctx, fld, cams, 0 * G)
     assert not g0.any()
     np.testing.assert_allclose(g2, 2 * g1, rtol=1e-4, atol=1e-6 * np.abs(g1).max())
+
+
+def test_renderer_api_matches_oracle(ctx):
+    """pipeline.Renderer (the UPDATE_GS building block): forward image equals
+    the oracle's; backward gradients match the float64 autograd oracle."""
+    import torch
+    import oracle
+    from paper_2602_15355_b200.pipeline import Renderer
+    from tests.gpu_utils import to_dev
+    fld, cams = synth.random_scene_small(7, 200, 48, 40, 45.0, 2, 3, logscale_mu=-2.4)
+    r = Renderer(to_dev(fld))
+    img = r.forward(cams)
+    ref_img = np.stack([oracle.render_view(fld, c)["rgbu"] for c in cams])
+    assert np.array_equal(img.cpu().numpy(), ref_img)
+    G = np.random.default_rng(8).normal(size=ref_img.shape).astype(np.float32)
+    got = r.backward(torch.from_numpy(G).cuda()).cpu().numpy()
+    _compare(got, bw.backward_views(fld, cams, G), 3)
