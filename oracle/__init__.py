@@ -86,6 +86,7 @@ def lib():
         L.orc_count_keys.restype = i64
         L.orc_emit_keys.argtypes = [P, i64, P, i32, P, P]
         L.orc_sort_pairs.argtypes = [P, P, i64]
+        L.orc_emit_keys_order.argtypes = [P, P, i64, P, i32, P, P]
         L.orc_ranges.argtypes = [P, i64, i64, P]
         L.orc_composite_tiled.argtypes = [P, P, P, P, P, P, P, P]
         L.orc_composite_tiled.restype = ctypes.c_double

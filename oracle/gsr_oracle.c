@@ -336,6 +336,31 @@ void orc_emit_keys(const orc_proj* p, int64_t n, const orc_camera* cam, int32_t 
   }
 }
 
+/* NEXT-2b: emit the keys of one view with the Gaussians visited in a given
+   order (the cached view-direction ordering) instead of by index: the low
+   32 bits of a key are the Gaussian's position in `order`, so the
+   (key, value) sort yields every tile's list in that order. */
+void orc_emit_keys_order(const orc_proj* p, const uint32_t* order, int64_t len, const orc_camera* cam,
+                         int32_t view_in_batch, uint64_t* keys, uint32_t* vals) {
+  uint64_t gx = (uint64_t)((cam->width + ORC_TILE - 1) / ORC_TILE);
+  uint64_t gy = (uint64_t)((cam->height + ORC_TILE - 1) / ORC_TILE);
+  int64_t k = 0;
+  for (int64_t i = 0; i < len; ++i) {
+    uint32_t g = order[i];
+    if (p[g].n_tiles == 0) continue;
+    for (uint32_t ty = p[g].py0 >> 4; ty <= (p[g].py1 >> 4); ++ty) {
+      uint32_t x0, x1;
+      orc_row_span(&p[g], ty, cam->width, &x0, &x1);
+      for (uint32_t tx = x0; tx < x1; ++tx) {
+        uint64_t tile = (uint64_t)view_in_batch * gx * gy + (uint64_t)ty * gx + tx;
+        keys[k] = (tile << 32) | (uint64_t)i;
+        vals[k] = g;
+        ++k;
+      }
+    }
+  }
+}
+
 typedef struct { uint64_t key; uint32_t val; } orc_pair;
 
 static int cmp_pair(const void* a, const void* b) {

@@ -342,6 +342,22 @@ def gen_config4_lod(n_per_tile: int = 500_000):
                                           LOD_THRESHOLDS)
 
 
+def config4_tiles(n_per_tile: int = 500_000, lod: bool = False):
+    """NEXT-2b tile structure of configs[3]: (tile_start int64 [17], centres
+    float64 [16][3]) of the 16 placed tiles in field order (row j, column i);
+    with ``lod`` the six levels of a placement are contiguous."""
+    per = sum(max(1, n_per_tile // LOD_COUNT_STEP ** l) for l in range(LOD_LEVELS)) if lod else n_per_tile
+    start = np.arange(17, dtype=np.int64) * per
+    centres = np.array([[i + 0.5, 0.0, j + 0.5] for j in range(4) for i in range(4)], dtype=np.float64)
+    return start, centres
+
+
+def tile_mean_uncertainty(field, tile_start) -> np.ndarray:
+    """Mean per-Gaussian uncertainty of each tile (the cache policy input)."""
+    u = field.planes[1, :, 3].astype(np.float64)
+    return np.array([u[tile_start[t]:tile_start[t + 1]].mean() for t in range(len(tile_start) - 1)])
+
+
 def random_lod(rng, n: int, levels: int = 4, thresholds=(1.0, 2.0, 3.0), delta: float = 0.3,
                centre_range: float = 1.5) -> LodData:
     """Random tile centres and levels for parity tests."""
