@@ -215,73 +215,54 @@ def bench_sobel(gsr, dev, peaks, reps: int = 20):
                          "unit": "GB/s", "frac": round(byts / t / 1e9 / peaks["hbm_gbs"], 4)}}
 
 
-def bench_lod(dev, steps: int = 3):
-    """NEXT-2: LOD blending (PAPER.md eq:lod_blend) on the config-4 fly-over
-    (64 views, 1920x1080): the 4x4 Wang assembly with six LOD levels per tile
-    (10.7 M Gaussians, K1 scales opacities by the level weights and culls the
-    inactive levels) vs the level-0-only assembly (8 M Gaussians, configs[3])."""
+def bench_wang(dev, steps: int = 3):
+    """NEXT-2 on the config-4 fly-over (64 views, 1920x1080, the 4x4 Wang
+    assembly): (a) LOD blending (PAPER.md eq:lod_blend) -- six levels per tile
+    (10.7 M Gaussians; K1 scales opacities by the level weights and culls the
+    inactive levels) vs the level-0-only assembly (8 M, configs[3]); (b) the
+    uncertainty-guided cached view-direction orderings (§3.5) replacing
+    the per-view depth sort, with the mean relative score change vs exact."""
     import torch
     import synth
     from paper_2602_15355_b200 import Gaussians, Lod
-    from paper_2602_15355_b200.pipeline import ViewScorer
+    from paper_2602_15355_b200.pipeline import ViewScorer, cache_bins
     cams = synth.flyover_cameras(64, 1920, 1080, 1500.0)
     out = {"config": "c4 fly-over 64 views 1920x1080; LOD: 6 levels/tile (1/4 count, 2.3x scale per level), "
-                      "D = 1.5, 3, 6, 12, 24, delta = 0.25"}
+                      "D = 1.5, 3, 6, 12, 24, delta = 0.25; cache: 8/16 azimuthal bins per tile (tau = 0.6)"}
 
-    def run(fld, lod):
-        G = Gaussians(torch.from_numpy(fld.planes).to(dev), fld.sh_degree)
-        L = None if lod is None else Lod(torch.from_numpy(lod.tile_level).to(dev), lod.levels, lod.delta,
-                                         lod.thresholds)
-        sc = ViewScorer(G, batch_views=16, n_slots=2, lod=L)
+    def run(G, L, tiles):
+        sc = ViewScorer(G, batch_views=16, n_slots=2, lod=L, order_tiles=tiles)
         for _ in range(2):
-            sc.score_views(cams)
+            s = sc.score_views(cams)
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         for _ in range(steps):
-            sc.score_views(cams)
+            s = sc.score_views(cams)
         e1.record()
         torch.cuda.synchronize()
         t = e0.elapsed_time(e1) / steps / 1e3
-        return {"gaussians": fld.n, "views_per_sec": round(64 / t, 1), "ms_per_pass": round(t * 1e3, 2),
-                "keys_per_view": int(sum(sc.last_keys) / 64)}
+        return {"gaussians": G.n, "views_per_sec": round(64 / t, 1), "ms_per_pass": round(t * 1e3, 2),
+                "keys_per_view": int(sum(sc.last_keys) / 64)}, s
 
-    fld, lod = synth.gen_config4_lod(500_000)
-    out["lod"] = run(fld, lod)
-    del fld, lod
-    out["level0_only"] = run(synth.gen_config4_field(500_000), None)
-    torch.cuda.empty_cache()
+    for name, lod in (("level0_only", False), ("lod", True)):
+        if lod:
+            fld, ld = synth.gen_config4_lod(500_000)
+        else:
+            fld, ld = synth.gen_config4_field(500_000), None
+        start, centres = synth.config4_tiles(500_000, lod=lod)
+        G = Gaussians(torch.from_numpy(fld.planes).to(dev), fld.sh_degree)
+        del fld
+        L = None if ld is None else Lod(torch.from_numpy(ld.tile_level).to(dev), ld.levels, ld.delta, ld.thresholds)
+        exact, s_exact = run(G, L, None)
+        bins = cache_bins(G, start)
+        cached, s_cached = run(G, L, (start, bins, centres))
+        cached["bins"] = sorted(set(int(b) for b in bins))
+        cached["mean_rel_score_change_vs_exact"] = float(((s_cached - s_exact).abs() / s_exact).mean().item())
+        out[name] = {"exact_sort": exact, "cached_order": cached}
+        del G, L
+        torch.cuda.empty_cache()
     return out
-
-
-def bench_backward(G, dev, reps: int = 3):
-    """NEXT-3: forward images + backward rasterizer for one 16-view c3 batch
-    (1 M Gaussians, 800x800), upstream gradient of an L2 photometric loss
-    against a perturbed copy of the image; device time per view."""
-    import torch
-    import synth
-    from paper_2602_15355_b200.pipeline import Renderer
-    cams = synth.fibonacci_cameras(1024, 4.0, 800, 800, 900.0)[::64]
-    r = Renderer(G)
-    img = r.forward(cams)
-    target = img + 0.01 * torch.randn_like(img)
-    grads = torch.zeros_like(G.planes)
-    e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
-    fw = bw = 0.0
-    for i in range(reps + 1):
-        e[0].record()
-        img = r.forward(cams)
-        e[1].record()
-        r.backward(2.0 * (img - target), grads)
-        e[2].record()
-        torch.cuda.synchronize()
-        if i:
-            fw += e[0].elapsed_time(e[1])
-            bw += e[1].elapsed_time(e[2])
-    fw, bw = fw / reps, bw / reps
-    return {"metric": "forward_backward_views_per_sec", "value": round(16 / ((fw + bw) / 1e3), 1), "unit": "views/s",
-            "forward_ms_per_batch": round(fw, 3), "backward_ms_per_batch": round(bw, 3),
-            "config": "c3 field (1M Gaussians, SH 3), 16 views 800x800, L2 loss vs a perturbed image"}
 
 
 # ----------------------------------------------------------------------------- GPU arm
@@ -441,7 +422,7 @@ def main():
         line["next1_w2"] = bench_w2(gsr, dev, peaks)
         line["next4_sobel"] = bench_sobel(gsr, dev, peaks)
         line["next3_backward"] = bench_backward(G, dev)
-        line["next2_lod"] = bench_lod(dev)
+        line["next2_wang"] = bench_wang(dev)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(scene, args.cpu_views)
     if rank == 0:

@@ -174,6 +174,36 @@ gsr_status gsr_bin_sort(gsr_ctx* ctx, const uint32_t* bin_rec, int64_t n, const 
                         int64_t* n_keys, uint32_t* ranges, uint64_t* keys_unsorted,
                         uint32_t* vals_unsorted, void* stream);
 
+/* ---- NEXT-2b: uncertainty-guided cached view-direction orderings ---------
+   (§3.5: "multiple view-dependent Gaussian orderings are
+   pre-sorted and cached per tile ... tiles with mean uncertainty above a
+   threshold tau retain a larger set of cached orderings").  A tile is a
+   contiguous index range [tile_start[t], tile_start[t+1]) of the field
+   (tile_start [host] int64 [n_tiles + 1], covering [0, n)); bins [host] int32
+   [n_tiles] = the tile's number of azimuthal bins (DESIGN.md policy: 16 if
+   its mean uncertainty > tau = 0.6, else 8).  Bin k of tile t orders the
+   tile's Gaussians by ascending fl32(fl32(x bx) + fl32(z bz)),
+   (bx, bz) = float32(cos, sin)(2 pi k / bins[t]), ties by index.
+   gsr_order_cache_size: elements of the cache = sum_t bins[t] n_t (host only).
+   gsr_build_order_cache: cache [device uint32, that size] = the orderings,
+     tile-major then bin-major (global Gaussian indices); once per field.
+   gsr_bin_sort_cached: gsr_bin_sort with the per-view depth sort replaced by
+     the cached order: per view (host, double) every tile takes the bin
+     maximising <h, b_k> (h = the horizontal part of the camera's forward
+     direction, ties to the lower k) and the tiles are visited front to back
+     by <centre - eye, forward> (centres [host] double [n_tiles][3], ties to
+     the lower tile); the visible Gaussians are emitted in that order, so every
+     tile list is composited in it (approximate: not the exact depth order).
+     Same outputs and errors as gsr_bin_sort (keys: low word = depth bits). */
+int64_t gsr_order_cache_size(const int64_t* tile_start, int32_t n_tiles, const int32_t* bins);
+gsr_status gsr_build_order_cache(gsr_ctx* ctx, const gsr_gaussians* gaussians, const int64_t* tile_start,
+                                 int32_t n_tiles, const int32_t* bins, uint32_t* cache, void* stream);
+gsr_status gsr_bin_sort_cached(gsr_ctx* ctx, const uint32_t* bin_rec, int64_t n, const gsr_camera* cams,
+                               int32_t n_views, const uint32_t* cache, const int64_t* tile_start,
+                               int32_t n_tiles, const int32_t* bins, const double* centres, uint64_t* keys,
+                               uint32_t* vals, int64_t capacity, int64_t* n_keys, uint32_t* ranges,
+                               void* stream);
+
 /* ---- K6: per-pixel front-to-back compositing of RGB + uncertainty ---------
    For pixel (px, py) of view c, over its tile's sorted list: alpha =
    min(0.99, o exp(power)), skip power > 0 or alpha < 1/255, stop before the

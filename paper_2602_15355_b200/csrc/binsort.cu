@@ -27,6 +27,9 @@
 #include "gsr_internal.cuh"
 
 #include <algorithm>
+#include <cmath>
+#include <string>
+#include <vector>
 
 namespace gsr {
 namespace {
@@ -993,6 +996,115 @@ __global__ void __launch_bounds__(256) k_emit_o2(const uint32_t* __restrict__ de
   }
 }
 
+// ---------------------------------------------------------------------------
+// NEXT-2b: compaction in the cached blend order.  Element i of view v is the
+// p-th Gaussian of the view's visiting sequence: the segment (tile in visit
+// order) holding p maps it to cache[off + p - start].  Visible ones are
+// compacted in that order into (view << 32, g) pairs -- the input K3 expects
+// -- so the per-view depth sort is skipped.
+struct OrderSeg {
+  uint64_t off;      // cache offset of the tile's chosen ordering
+  uint32_t start;    // first sequence position of the tile
+  uint32_t len;      // Gaussians in the tile
+};
+
+__global__ void __launch_bounds__(256) k2c_compact(const OrderSeg* __restrict__ segs, int n_seg,
+                                                   const uint32_t* __restrict__ cache,
+                                                   const uint32_t* __restrict__ nt_plane, int64_t M, int64_t n,
+                                                   uint64_t* __restrict__ dkeys, uint32_t* __restrict__ dvals,
+                                                   uint64_t* __restrict__ lb_vis, uint64_t* __restrict__ lb_k,
+                                                   uint32_t* __restrict__ ctr, uint64_t* __restrict__ totals) {
+  __shared__ uint64_t s_wv[8], s_wk[8];
+  __shared__ uint64_t s_pv;
+  __shared__ uint32_t s_bid;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) s_bid = atomicAdd(ctr, 1u);
+  __syncthreads();
+  const int64_t bid = s_bid;
+  const int64_t i0 = bid * K2_TILE + (int64_t)tid * K2_ITEMS;
+  uint32_t nt[K2_ITEMS], gg[K2_ITEMS];
+  uint32_t cv = 0;
+  uint64_t ck = 0;
+#pragma unroll
+  for (int k = 0; k < K2_ITEMS; ++k) {
+    nt[k] = 0;
+    gg[k] = 0;
+    const int64_t i = i0 + k;
+    if (i < M) {
+      const int64_t view = i / n;
+      const uint32_t p = (uint32_t)(i - view * n);
+      const OrderSeg* S = segs + view * n_seg;
+      int lo = 0, hi = n_seg - 1;  // last segment with start <= p
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (S[mid].start <= p) lo = mid; else hi = mid - 1;
+      }
+      const uint32_t g = __ldg(cache + S[lo].off + (p - S[lo].start));
+      gg[k] = g;
+      nt[k] = __ldg(nt_plane + view * n + g);
+    }
+    cv += nt[k] > 0;
+    ck += nt[k];
+  }
+  uint64_t iv = warp_incl_scan<uint64_t>(cv), ik = warp_incl_scan<uint64_t>(ck);
+  if (lane == 31) { s_wv[warp] = iv; s_wk[warp] = ik; }
+  __syncthreads();
+  if (warp == 0) {
+    uint64_t wv = lane < 8 ? s_wv[lane] : 0, wk = lane < 8 ? s_wk[lane] : 0;
+    uint64_t sv = warp_incl_scan<uint64_t>(wv), sk = warp_incl_scan<uint64_t>(wk);
+    if (lane < 8) { s_wv[lane] = sv - wv; s_wk[lane] = sk - wk; }
+    const uint64_t tv = __shfl_sync(FULL, sv, 7), tk = __shfl_sync(FULL, sk, 7);
+    uint64_t pv = 0, pk = 0;
+    if (bid == 0) {
+      if (lane == 0) { publish(lb_vis, 0, LB_INC | tv); publish(lb_k, 0, LB_INC | tk); }
+    } else {
+      if (lane == 0) { publish(lb_vis, bid, LB_AGG | tv); publish(lb_k, bid, LB_AGG | tk); }
+      pv = warp_lookback(lb_vis, bid);
+      pk = warp_lookback(lb_k, bid);
+      if (lane == 0) { publish(lb_vis, bid, LB_INC | (pv + tv)); publish(lb_k, bid, LB_INC | (pk + tk)); }
+    }
+    if (lane == 0) {
+      s_pv = pv;
+      if ((bid + 1) * K2_TILE >= M) { totals[0] = pv + tv; totals[1] = pk + tk; }
+    }
+  }
+  __syncthreads();
+  uint64_t pv = s_pv + s_wv[warp] + (iv - cv);
+#pragma unroll
+  for (int k = 0; k < K2_ITEMS; ++k) {
+    const int64_t i = i0 + k;
+    if (i >= M) break;
+    if (nt[k]) {
+      dkeys[pv] = (uint64_t)(i / n) << 32;
+      dvals[pv] = gg[k];
+      ++pv;
+    }
+  }
+}
+
+// NEXT-2b cache build: key of element i of segment s = (t, k) is
+// (s << 32) | orderable(fl32(fl32(x bx) + fl32(z bz))), value = g.
+struct CacheSeg {
+  uint64_t out;      // first cache slot of the segment
+  uint32_t start;    // first Gaussian of the tile
+  uint32_t len;
+  float bx, bz;
+};
+
+__global__ void __launch_bounds__(256) kc_keys(const CacheSeg* __restrict__ segs, const float4* __restrict__ po,
+                                               uint64_t* __restrict__ keys, uint32_t* __restrict__ vals) {
+  const CacheSeg sg = segs[blockIdx.y];
+  for (uint32_t i = blockIdx.x * 256 + threadIdx.x; i < sg.len; i += gridDim.x * 256) {
+    const uint32_t g = sg.start + i;
+    const float4 P = __ldg(po + g);
+    const float key = (P.x * sg.bx) + (P.z * sg.bz);
+    uint32_t b = __float_as_uint(key);
+    b = (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+    keys[sg.out + i] = ((uint64_t)blockIdx.y << 32) | b;
+    vals[sg.out + i] = g;
+  }
+}
+
 int bits_for(uint64_t count) {  // ceil(log2(count)), 0 for count <= 1
   int b = 0;
   while ((1ull << b) < count) ++b;
@@ -1132,10 +1244,16 @@ extern "C" gsr_status gsr_sort_pairs_u64(gsr_ctx* ctx, const uint64_t* keys_in, 
                          end_bit, base, look, ctrs, st);
 }
 
-extern "C" gsr_status gsr_bin_sort(gsr_ctx* ctx, const uint32_t* bin_rec, int64_t n, const gsr_camera* cams,
-                                   int32_t n_views, uint64_t* keys, uint32_t* vals, int64_t capacity,
-                                   int64_t* n_keys, uint32_t* ranges, uint64_t* keys_unsorted,
-                                   uint32_t* vals_unsorted, void* stream) {
+struct CachedOrder {  // NEXT-2b: device visiting table [V][n_seg] + cache
+  const OrderSeg* segs;
+  int n_seg;
+  const uint32_t* cache;
+};
+
+static gsr_status bin_sort_impl(gsr_ctx* ctx, const uint32_t* bin_rec, int64_t n, const gsr_camera* cams,
+                                int32_t n_views, uint64_t* keys, uint32_t* vals, int64_t capacity, int64_t* n_keys,
+                                uint32_t* ranges, uint64_t* keys_unsorted, uint32_t* vals_unsorted,
+                                const CachedOrder* co, void* stream) {
   if (!ctx) return GSR_EINVAL;
   if (!bin_rec || !cams || !vals || !n_keys || !ranges)
     return set_err(ctx, GSR_EINVAL, "gsr_bin_sort: NULL required pointer");
@@ -1190,9 +1308,12 @@ extern "C" gsr_status gsr_bin_sort(gsr_ctx* ctx, const uint32_t* bin_rec, int64_
   uint64_t* lbk = lbv + std::max<size_t>(nb2, 1);
   uint32_t* ctr2 = (uint32_t*)((char*)lb + align_up(2 * std::max<size_t>(nb2, 1) * 8));
   const int sp2 = stage_begin(ctx, GSR_STAGE_COMPACT, st);
-  if (M > 0)
+  if (M > 0 && !co)
     k2_compact<<<(unsigned)nb2, 256, 0, st>>>(p_depth, p_nt, M, n, (uint64_t*)dka, (uint32_t*)dva,
                                               (uint32_t*)eo, lbv, lbk, ctr2, (uint64_t*)tot, dhist, dpasses);
+  if (M > 0 && co)
+    k2c_compact<<<(unsigned)nb2, 256, 0, st>>>(co->segs, co->n_seg, co->cache, p_nt, M, n, (uint64_t*)dka,
+                                               (uint32_t*)dva, lbv, lbk, ctr2, (uint64_t*)tot);
   stage_end(ctx, sp2, st);
   if ((s = check_cuda(ctx, cudaGetLastError(), "k2_compact")) != GSR_OK) return s;
   uint64_t* hp = (uint64_t*)ctx->host_pinned;
@@ -1207,7 +1328,7 @@ extern "C" gsr_status gsr_bin_sort(gsr_ctx* ctx, const uint32_t* bin_rec, int64_
   // algorithmic bytes: K2 reads n_tiles of every pair and the depth of
   // the visible ones, writes 12 B per visible pair; K1's 48-B render records of
   // the visible pairs are attributed to the projection stage.
-  account(ctx, GSR_STAGE_COMPACT, M > 0 ? 1 : 0, 4.0 * M + 16.0 * nvis);
+  account(ctx, GSR_STAGE_COMPACT, M > 0 ? 1 : 0, (co ? 8.0 : 4.0) * M + 12.0 * nvis + (co ? 0.0 : 4.0 * nvis));
   account(ctx, GSR_STAGE_PROJECT, 0, 80.0 * nvis);
   if (K > capacity) return set_err(ctx, GSR_ECAPACITY, "gsr_bin_sort: capacity too small (n_keys = required)");
   if (K >= (1ll << 31)) return set_err(ctx, GSR_EINVAL, "gsr_bin_sort: K >= 2^31 keys in one batch");
@@ -1245,28 +1366,30 @@ extern "C" gsr_status gsr_bin_sort(gsr_ctx* ctx, const uint32_t* bin_rec, int64_
   uint32_t* lbt = (uint32_t*)((char*)lb + o_t);
   uint32_t* ctrs = (uint32_t*)((char*)lb + o_c);  // [0..4] depth, [5] k3, [6..9] tile
 
-  // ---- K4a: depth sort of the visible pairs ----
-  int sp = stage_begin(ctx, GSR_STAGE_DEPTH_SORT, st);
-  scan_hist<<<1, 256, 0, st>>>(dhist, dbase, dpasses);
+  // ---- K4a: depth sort of the visible pairs (skipped in the cached order) ----
   const uint64_t* ck = (const uint64_t*)dka;
   const uint32_t* cvv = (const uint32_t*)dva;
-  for (int p = 0; p < dpasses; ++p) {
-    uint64_t* ko = (p % 2 == 0) ? (uint64_t*)dkb : (uint64_t*)dka;
-    uint32_t* vo = (p % 2 == 0) ? (uint32_t*)dvb : (uint32_t*)dva;
-    const int sh = 8 * p;
-    cudaError_t e = run_pass<uint64_t, 0>(variant, ctx->num_sms, ck, cvv, ko, vo, (uint32_t)nvis, sh,
-                                          std::min(8, 32 + vbits - sh), dbase + 256 * p,
-                                          lbd + (size_t)p * nbd * 256, ctrs + p, nullptr, nullptr, 0, 0, st);
-    if ((s = check_cuda(ctx, e, "depth sort pass")) != GSR_OK) return s;
-    ck = ko;
-    cvv = vo;
+  if (!co) {
+    int spd = stage_begin(ctx, GSR_STAGE_DEPTH_SORT, st);
+    scan_hist<<<1, 256, 0, st>>>(dhist, dbase, dpasses);
+    for (int p = 0; p < dpasses; ++p) {
+      uint64_t* ko = (p % 2 == 0) ? (uint64_t*)dkb : (uint64_t*)dka;
+      uint32_t* vo = (p % 2 == 0) ? (uint32_t*)dvb : (uint32_t*)dva;
+      const int sh = 8 * p;
+      cudaError_t e = run_pass<uint64_t, 0>(variant, ctx->num_sms, ck, cvv, ko, vo, (uint32_t)nvis, sh,
+                                            std::min(8, 32 + vbits - sh), dbase + 256 * p,
+                                            lbd + (size_t)p * nbd * 256, ctrs + p, nullptr, nullptr, 0, 0, st);
+      if ((s = check_cuda(ctx, e, "depth sort pass")) != GSR_OK) return s;
+      ck = ko;
+      cvv = vo;
+    }
+    stage_end(ctx, spd, st);
+    account(ctx, GSR_STAGE_DEPTH_SORT, 1 + dpasses * pass_launches(variant), 24.0 * dpasses * nvis);
+    if ((s = check_cuda(ctx, cudaGetLastError(), "depth sort")) != GSR_OK) return s;
   }
-  stage_end(ctx, sp, st);
-  account(ctx, GSR_STAGE_DEPTH_SORT, 1 + dpasses * pass_launches(variant), 24.0 * dpasses * nvis);
-  if ((s = check_cuda(ctx, cudaGetLastError(), "depth sort")) != GSR_OK) return s;
 
   // ---- K3: emission + counts ----
-  sp = stage_begin(ctx, GSR_STAGE_EMIT, st);
+  int sp = stage_begin(ctx, GSR_STAGE_EMIT, st);
   const int bins = tpv <= 12288 ? (int)tpv : 0;  // <= 48 KB of shared memory
   k3_emit<<<(unsigned)nb3, 256, bins * 4, st>>>(ck, cvv, nvis, p_span, n, gx, (uint32_t)tpv, W, (uint32_t*)tka,
                                                 (uint32_t*)tva, (uint32_t*)cnt, lb3, ctrs + 5, bins);
@@ -1318,4 +1441,140 @@ extern "C" gsr_status gsr_bin_sort(gsr_ctx* ctx, const uint32_t* bin_rec, int64_
     if ((s = check_cuda(ctx, cudaGetLastError(), "emit_o2")) != GSR_OK) return s;
   }
   return GSR_OK;
+}
+
+extern "C" gsr_status gsr_bin_sort(gsr_ctx* ctx, const uint32_t* bin_rec, int64_t n, const gsr_camera* cams,
+                                   int32_t n_views, uint64_t* keys, uint32_t* vals, int64_t capacity,
+                                   int64_t* n_keys, uint32_t* ranges, uint64_t* keys_unsorted,
+                                   uint32_t* vals_unsorted, void* stream) {
+  return bin_sort_impl(ctx, bin_rec, n, cams, n_views, keys, vals, capacity, n_keys, ranges, keys_unsorted,
+                       vals_unsorted, nullptr, stream);
+}
+
+// ---- NEXT-2b: cached view-direction orderings ----
+static gsr_status check_tiles(gsr_ctx* ctx, const int64_t* tile_start, int32_t n_tiles, const int32_t* bins,
+                              int64_t n, const char* who) {
+  if (!tile_start || !bins || n_tiles <= 0 || n_tiles > 4096)
+    return set_err(ctx, GSR_EINVAL, std::string(who) + ": bad tile table");
+  if (tile_start[0] != 0 || tile_start[n_tiles] != n)
+    return set_err(ctx, GSR_EINVAL, std::string(who) + ": tile ranges must cover [0, n)");
+  for (int t = 0; t < n_tiles; ++t) {
+    if (tile_start[t + 1] < tile_start[t]) return set_err(ctx, GSR_EINVAL, std::string(who) + ": tile ranges");
+    if (bins[t] < 1 || bins[t] > 64) return set_err(ctx, GSR_EINVAL, std::string(who) + ": bins in [1, 64]");
+  }
+  return GSR_OK;
+}
+
+extern "C" int64_t gsr_order_cache_size(const int64_t* tile_start, int32_t n_tiles, const int32_t* bins) {
+  if (!tile_start || !bins || n_tiles <= 0) return 0;
+  int64_t s = 0;
+  for (int t = 0; t < n_tiles; ++t) s += (int64_t)bins[t] * (tile_start[t + 1] - tile_start[t]);
+  return s;
+}
+
+extern "C" gsr_status gsr_build_order_cache(gsr_ctx* ctx, const gsr_gaussians* G, const int64_t* tile_start,
+                                            int32_t n_tiles, const int32_t* bins, uint32_t* cache, void* stream) {
+  if (!ctx) return GSR_EINVAL;
+  if (!G || !cache) return set_err(ctx, GSR_EINVAL, "gsr_build_order_cache: NULL required pointer");
+  gsr_status s;
+  if ((s = check_tiles(ctx, tile_start, n_tiles, bins, G->n, "gsr_build_order_cache")) != GSR_OK) return s;
+  std::vector<CacheSeg> segs;
+  uint64_t out = 0;
+  uint32_t maxlen = 0;
+  for (int t = 0; t < n_tiles; ++t) {
+    const uint32_t len = (uint32_t)(tile_start[t + 1] - tile_start[t]);
+    maxlen = std::max(maxlen, len);
+    for (int k = 0; k < bins[t]; ++k) {
+      const double a = 2.0 * M_PI * k / bins[t];
+      segs.push_back(CacheSeg{out, (uint32_t)tile_start[t], len, (float)std::cos(a), (float)std::sin(a)});
+      out += len;
+    }
+  }
+  const int64_t N = (int64_t)out;
+  if (N == 0) return GSR_OK;
+  if (N >= (1ll << 31)) return set_err(ctx, GSR_EINVAL, "gsr_build_order_cache: cache too large");
+  cudaStream_t st = (cudaStream_t)stream;
+  // the bin-sort scratch slots hold the sort input / key output (the utility
+  // sort's own temporaries live in S_SORTK / S_SORTV)
+  void *tab, *k0, *k1, *v0;
+  const size_t tb = segs.size() * sizeof(CacheSeg);
+  if ((s = ensure(ctx, S_SELECT2, tb, &tab)) != GSR_OK) return s;
+  if ((s = ensure(ctx, S_DKEY_A, (size_t)N * 8, &k0)) != GSR_OK) return s;
+  if ((s = ensure(ctx, S_DKEY_B, (size_t)N * 8, &k1)) != GSR_OK) return s;
+  if ((s = ensure(ctx, S_DVAL_A, (size_t)N * 4, &v0)) != GSR_OK) return s;
+  if ((s = check_cuda(ctx, cudaMemcpyAsync(tab, segs.data(), tb, cudaMemcpyHostToDevice, st), "segs")) != GSR_OK)
+    return s;
+  uint64_t* keys = (uint64_t*)k0;
+  uint64_t* keys_out = (uint64_t*)k1;
+  uint32_t* vals = (uint32_t*)v0;
+  const dim3 grid((unsigned)std::min<uint32_t>((maxlen + 255) / 256, 1024), (unsigned)segs.size());
+  kc_keys<<<grid, 256, 0, st>>>((const CacheSeg*)tab, reinterpret_cast<const float4*>(G->pos_opacity), keys, vals);
+  if ((s = check_cuda(ctx, cudaGetLastError(), "kc_keys")) != GSR_OK) return s;
+  // stable sort by (segment, key): the sorted values are the cache
+  const int end_bit = 32 + std::max(1, bits_for(segs.size()));
+  return gsr_sort_pairs_u64(ctx, keys, vals, keys_out, cache, N, 0, end_bit, stream);
+}
+
+extern "C" gsr_status gsr_bin_sort_cached(gsr_ctx* ctx, const uint32_t* bin_rec, int64_t n, const gsr_camera* cams,
+                                          int32_t n_views, const uint32_t* cache, const int64_t* tile_start,
+                                          int32_t n_tiles, const int32_t* bins, const double* centres,
+                                          uint64_t* keys, uint32_t* vals, int64_t capacity, int64_t* n_keys,
+                                          uint32_t* ranges, void* stream) {
+  if (!ctx) return GSR_EINVAL;
+  if (!cache || !centres || !cams) return set_err(ctx, GSR_EINVAL, "gsr_bin_sort_cached: NULL required pointer");
+  if (n_views <= 0 || n_views > GSR_MAX_VIEWS) return set_err(ctx, GSR_EINVAL, "gsr_bin_sort_cached: bad n_views");
+  gsr_status s;
+  if ((s = check_tiles(ctx, tile_start, n_tiles, bins, n, "gsr_bin_sort_cached")) != GSR_OK) return s;
+  // per view: the chosen bin of every tile and the tiles' visiting order (host, double)
+  std::vector<uint64_t> base(n_tiles);
+  uint64_t off = 0;
+  for (int t = 0; t < n_tiles; ++t) {
+    base[t] = off;
+    off += (uint64_t)bins[t] * (uint64_t)(tile_start[t + 1] - tile_start[t]);
+  }
+  std::vector<OrderSeg> segs((size_t)n_views * n_tiles);
+  std::vector<int> order(n_tiles);
+  std::vector<double> depth(n_tiles);
+  for (int v = 0; v < n_views; ++v) {
+    const gsr_camera& c = cams[v];
+    const double f[3] = {c.R[6], c.R[7], c.R[8]};
+    const double eye[3] = {c.campos[0], c.campos[1], c.campos[2]};
+    double h0 = f[0], h1 = f[2];
+    const double hn = std::max(std::sqrt(h0 * h0 + h1 * h1), 1e-30);
+    h0 /= hn;
+    h1 /= hn;
+    for (int t = 0; t < n_tiles; ++t) {
+      depth[t] = ((centres[3 * t] - eye[0]) * f[0] + (centres[3 * t + 1] - eye[1]) * f[1]) +
+                 (centres[3 * t + 2] - eye[2]) * f[2];
+      order[t] = t;
+    }
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return depth[a] < depth[b]; });
+    uint32_t pos = 0;
+    for (int i = 0; i < n_tiles; ++i) {
+      const int t = order[i];
+      int best = 0;
+      double bd = -1e300;
+      for (int k = 0; k < bins[t]; ++k) {
+        const double a = 2.0 * M_PI * k / bins[t];
+        const double d = h0 * std::cos(a) + h1 * std::sin(a);
+        if (d > bd) {
+          bd = d;
+          best = k;
+        }
+      }
+      const uint32_t len = (uint32_t)(tile_start[t + 1] - tile_start[t]);
+      segs[(size_t)v * n_tiles + i] = OrderSeg{base[t] + (uint64_t)best * len, pos, len};
+      pos += len;
+    }
+  }
+  void* tab;
+  const size_t tb = segs.size() * sizeof(OrderSeg);
+  if ((s = ensure(ctx, S_SELECT2, tb, &tab)) != GSR_OK) return s;
+  cudaStream_t st = (cudaStream_t)stream;
+  if ((s = check_cuda(ctx, cudaMemcpyAsync(tab, segs.data(), tb, cudaMemcpyHostToDevice, st), "order table")) !=
+      GSR_OK)
+    return s;
+  CachedOrder co{(const OrderSeg*)tab, n_tiles, cache};
+  return bin_sort_impl(ctx, bin_rec, n, cams, n_views, keys, vals, capacity, n_keys, ranges, nullptr, nullptr, &co,
+                       stream);
 }

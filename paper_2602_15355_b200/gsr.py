@@ -32,7 +32,8 @@ assert CAM_DTYPE.itemsize == 96
 EXPORTED = ["gsr_create", "gsr_destroy", "gsr_last_error", "gsr_version", "gsr_camera_look_at",
             "gsr_project", "gsr_bin_sort", "gsr_composite", "gsr_score_views", "gsr_select_nbv",
             "gsr_sort_pairs_u64", "gsr_scratch_bytes", "gsr_timing_enable", "gsr_timing_read", "gsr_w2_scores",
-            "gsr_sobel_scores", "gsr_backward"]
+            "gsr_sobel_scores", "gsr_backward", "gsr_order_cache_size", "gsr_build_order_cache",
+            "gsr_bin_sort_cached"]
 STAGES = ["project", "compact", "depth_sort", "emit", "ranges", "tile_sort", "composite", "score", "select",
           "sort_u64", "w2", "sobel", "backward"]
 
@@ -71,6 +72,10 @@ def _load():
     L.gsr_composite.argtypes = [P, P, i64, P, P, P, i32, P, P, P, P, P, P, P]
     L.gsr_sobel_scores.argtypes = [P, P, P, i32, P, P, P]
     L.gsr_backward.argtypes = [P, P, P, i32, P, P, P, P, P, P, P, P, P]
+    L.gsr_order_cache_size.argtypes = [P, i32, P]
+    L.gsr_order_cache_size.restype = i64
+    L.gsr_build_order_cache.argtypes = [P, P, P, i32, P, P, P]
+    L.gsr_bin_sort_cached.argtypes = [P, P, i64, P, i32, P, P, i32, P, P, P, P, i64, P, P, P]
     L.gsr_score_views.argtypes = [P, P, P, i32, P, P]
     L.gsr_select_nbv.argtypes = [P, P, i32, P, i32, P, P]
     L.gsr_sort_pairs_u64.argtypes = [P, P, P, P, P, i64, i32, i32, P]
@@ -80,7 +85,7 @@ def _load():
     L.gsr_scratch_bytes.argtypes = [P]
     L.gsr_scratch_bytes.restype = i64
     for name in EXPORTED:
-        if name not in ("gsr_last_error", "gsr_version", "gsr_scratch_bytes"):
+        if name not in ("gsr_last_error", "gsr_version", "gsr_scratch_bytes", "gsr_order_cache_size"):
             getattr(L, name).restype = st
     return L
 
@@ -217,6 +222,41 @@ def gsr_bin_sort(ctx: Context, bin_rec, n: int, cams, vals, capacity: int, range
     st = lib.gsr_bin_sort(ctx.handle, _ptr(bin_rec), n, c.ctypes.data, len(c), _ptr(keys), _ptr(vals), capacity,
                           ctypes.byref(nk), _ptr(ranges), _ptr(keys_unsorted), _ptr(vals_unsorted),
                           _stream(stream))
+    if st == GSR_ECAPACITY:
+        e = GsrError(st, lib.gsr_last_error(ctx.handle).decode())
+        e.required = int(nk.value)
+        raise e
+    ctx._check(st)
+    return int(nk.value)
+
+
+class OrderCache:
+    """NEXT-2b: the field's cached view-direction orderings (device) + the
+    tile table (host): tile_start int64 [n_tiles + 1], bins int32 [n_tiles],
+    centres float64 [n_tiles][3]."""
+
+    def __init__(self, ctx: "Context", g: Gaussians, tile_start, bins, centres, stream=None):
+        import torch
+        self.tile_start = np.ascontiguousarray(np.asarray(tile_start, dtype=np.int64))
+        self.bins = np.ascontiguousarray(np.asarray(bins, dtype=np.int32))
+        self.centres = np.ascontiguousarray(np.asarray(centres, dtype=np.float64).reshape(-1, 3))
+        self.n_tiles = len(self.bins)
+        size = int(lib.gsr_order_cache_size(self.tile_start.ctypes.data, self.n_tiles, self.bins.ctypes.data))
+        self.cache = torch.empty(max(size, 1), dtype=torch.int32, device=g.planes.device)
+        gs = g.struct()
+        ctx._check(lib.gsr_build_order_cache(ctx.handle, ctypes.byref(gs), self.tile_start.ctypes.data,
+                                             self.n_tiles, self.bins.ctypes.data, _ptr(self.cache),
+                                             _stream(stream)))
+
+
+def gsr_bin_sort_cached(ctx: Context, bin_rec, n: int, cams, oc: OrderCache, vals, capacity: int, ranges,
+                        keys=None, stream=None) -> int:
+    """gsr_bin_sort with the cached blend order (NEXT-2b); returns K."""
+    c = cams_array(cams)
+    nk = ctypes.c_int64(0)
+    st = lib.gsr_bin_sort_cached(ctx.handle, _ptr(bin_rec), n, c.ctypes.data, len(c), _ptr(oc.cache),
+                                 oc.tile_start.ctypes.data, oc.n_tiles, oc.bins.ctypes.data, oc.centres.ctypes.data,
+                                 _ptr(keys), _ptr(vals), capacity, ctypes.byref(nk), _ptr(ranges), _stream(stream))
     if st == GSR_ECAPACITY:
         e = GsrError(st, lib.gsr_last_error(ctx.handle).decode())
         e.required = int(nk.value)

@@ -22,6 +22,21 @@ from . import gsr
 from .gsr import Context, Gaussians, GsrError
 
 
+CACHE_TAU, CACHE_BASE_BINS, CACHE_HOT_BINS = 0.6, 8, 16
+
+
+def cache_bins(field: Gaussians, tile_start, tau: float = CACHE_TAU) -> np.ndarray:
+    """NEXT-2b cache policy (§3.5, tau = 0.6 of §3.6):
+    a tile whose mean per-Gaussian uncertainty exceeds tau keeps 16 cached
+    orderings, the others 8."""
+    u = field.planes[1, :, 3]
+    out = []
+    for t in range(len(tile_start) - 1):
+        m = float(u[int(tile_start[t]):int(tile_start[t + 1])].double().mean().item())
+        out.append(CACHE_HOT_BINS if m > tau else CACHE_BASE_BINS)
+    return np.asarray(out, dtype=np.int32)
+
+
 def tiles_per_view(cam) -> int:
     W, H = int(cam["width"]), int(cam["height"])
     return ((W + 15) // 16) * ((H + 15) // 16)
@@ -65,9 +80,12 @@ class ViewScorer:
     capacity follows gsr_bin_sort's capacity protocol (GSR_ECAPACITY returns
     the required size; grow by 25 % and retry)."""
 
-    def __init__(self, field: Gaussians, batch_views: int = 16, n_slots: int = 2, lod: Optional[gsr.Lod] = None):
+    def __init__(self, field: Gaussians, batch_views: int = 16, n_slots: int = 2, lod: Optional[gsr.Lod] = None,
+                 order_tiles=None):
         self.field = field
         self.lod = lod  # NEXT-2 LOD blending (opacity multiplier in K1), or None
+        # NEXT-2b: (tile_start, bins, centres) -> cached view-direction orderings
+        # replace the per-view depth sort (approximate blend order)
         self.dev = field.planes.device
         self.V = min(int(batch_views), gsr.GSR_MAX_VIEWS)
         self.slots: List[_Slot] = []
@@ -80,6 +98,10 @@ class ViewScorer:
                 self.slots.append(_Slot(self.dev, self.V, field.n, torch.cuda.Stream(self.dev)))
         self.ctx = self.slots[0].ctx
         self.last_keys: List[int] = []
+        self.order_cache = None
+        if order_tiles is not None:
+            self.order_cache = gsr.OrderCache(self.ctx, field, *order_tiles)
+            torch.cuda.synchronize(self.dev)
 
     # ------------------------------------------------------------------ helpers
     @property
@@ -168,8 +190,12 @@ class ViewScorer:
         gsr.gsr_project(S.ctx, self.field, cams, S.rec, S.bin, st, lod=self.lod)
         while True:
             try:
-                K = gsr.gsr_bin_sort(S.ctx, S.bin, n, cams, S.vals, S.capacity, S.ranges,
-                                     keys=S.keys if want_keys else None, stream=st)
+                if self.order_cache is not None:
+                    K = gsr.gsr_bin_sort_cached(S.ctx, S.bin, n, cams, self.order_cache, S.vals, S.capacity,
+                                                S.ranges, keys=S.keys if want_keys else None, stream=st)
+                else:
+                    K = gsr.gsr_bin_sort(S.ctx, S.bin, n, cams, S.vals, S.capacity, S.ranges,
+                                         keys=S.keys if want_keys else None, stream=st)
                 break
             except GsrError as e:
                 if e.status != gsr.GSR_ECAPACITY:
