@@ -265,6 +265,36 @@ def bench_wang(dev, steps: int = 3):
     return out
 
 
+def bench_backward(G, dev, reps: int = 3):
+    """NEXT-3: forward images + backward rasterizer for one 16-view c3 batch
+    (1 M Gaussians, 800x800), upstream gradient of an L2 photometric loss
+    against a perturbed copy of the image; device time per view."""
+    import torch
+    import synth
+    from paper_2602_15355_b200.pipeline import Renderer
+    cams = synth.fibonacci_cameras(1024, 4.0, 800, 800, 900.0)[::64]
+    r = Renderer(G)
+    img = r.forward(cams)
+    target = img + 0.01 * torch.randn_like(img)
+    grads = torch.zeros_like(G.planes)
+    e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+    fw = bw = 0.0
+    for i in range(reps + 1):
+        e[0].record()
+        img = r.forward(cams)
+        e[1].record()
+        r.backward(2.0 * (img - target), grads)
+        e[2].record()
+        torch.cuda.synchronize()
+        if i:
+            fw += e[0].elapsed_time(e[1])
+            bw += e[1].elapsed_time(e[2])
+    fw, bw = fw / reps, bw / reps
+    return {"metric": "forward_backward_views_per_sec", "value": round(16 / ((fw + bw) / 1e3), 1), "unit": "views/s",
+            "forward_ms_per_batch": round(fw, 3), "backward_ms_per_batch": round(bw, 3),
+            "config": "c3 field (1M Gaussians, SH 3), 16 views 800x800, L2 loss vs a perturbed image"}
+
+
 # ----------------------------------------------------------------------------- GPU arm
 def main():
     args = parse()

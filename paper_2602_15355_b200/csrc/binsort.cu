@@ -28,6 +28,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstring>
 #include <string>
 #include <vector>
 
@@ -129,13 +130,21 @@ __device__ __forceinline__ void publish(uint64_t* words, int64_t bid, uint64_t v
 constexpr int K2_ITEMS = 8;
 constexpr int K2_TILE = 256 * K2_ITEMS;
 
+// KeyT = uint64_t: key = view << 32 | depth bits.  KeyT = uint32_t (the
+// default): key = view << dshift | (depth bits - dbase) with dbase = the bits
+// of the batch's smallest znear (every visible depth is above it, and
+// positive float bits order like the floats); a depth whose offset needs more
+// than dshift bits raises totals[2] and the caller reruns with 64-bit keys.
+// Same order either way; the 32-bit keys halve the depth sort's traffic
+// (4 passes x 8 B instead of 5 x 12 B per visible pair).
+template <typename KeyT>
 __global__ void __launch_bounds__(256) k2_compact(const uint32_t* __restrict__ depth_plane,
                                                   const uint32_t* __restrict__ nt_plane, int64_t M, int64_t n,
-                                                  uint64_t* __restrict__ dkeys, uint32_t* __restrict__ dvals,
+                                                  KeyT* __restrict__ dkeys, uint32_t* __restrict__ dvals,
                                                   uint32_t* __restrict__ emit_off, uint64_t* __restrict__ lb_vis,
                                                   uint64_t* __restrict__ lb_k, uint32_t* __restrict__ ctr,
                                                   uint64_t* __restrict__ totals, uint32_t* __restrict__ hist,
-                                                  int dpasses) {
+                                                  int dpasses, int dshift, uint32_t dbase) {
   __shared__ uint32_t s_hist[5][256];
   __shared__ uint64_t s_wv[8], s_wk[8];
   __shared__ uint64_t s_pv, s_pk;
@@ -189,10 +198,18 @@ __global__ void __launch_bounds__(256) k2_compact(const uint32_t* __restrict__ d
     if (nt[k]) {
       const uint64_t view = (uint64_t)(i / n);
       const uint32_t g = (uint32_t)(i - (int64_t)view * n);
-      const uint64_t key = (view << 32) | __ldg(depth_plane + i);
+      const uint32_t d = __ldg(depth_plane + i);
+      KeyT key;
+      if (sizeof(KeyT) == 8) {
+        key = (KeyT)((view << 32) | d);
+      } else {
+        const uint32_t off = d - dbase;
+        if (off >> dshift) totals[2] = 1;  // does not fit: caller falls back to 64-bit keys
+        key = (KeyT)(((uint32_t)view << dshift) | off);
+      }
       dkeys[pv] = key;
       dvals[pv] = g;
-      for (int p = 0; p < dpasses; ++p) atomicAdd(&s_hist[p][(key >> (8 * p)) & 255], 1u);
+      for (int p = 0; p < dpasses; ++p) atomicAdd(&s_hist[p][(uint32_t)(key >> (8 * p)) & 255], 1u);
       ++pv;
     }
     pk += nt[k];
@@ -776,12 +793,13 @@ __device__ __forceinline__ int owner_of(uint32_t excl, uint32_t j) {  // largest
   return s;
 }
 
-__global__ void __launch_bounds__(256) k3_emit(const uint64_t* __restrict__ dkeys, const uint32_t* __restrict__ dvals,
+template <typename KeyT>
+__global__ void __launch_bounds__(256) k3_emit(const KeyT* __restrict__ dkeys, const uint32_t* __restrict__ dvals,
                                                int64_t nvis, const uint4* __restrict__ span, int64_t n, uint32_t gx,
                                                uint32_t tpv, int W, uint32_t* __restrict__ tkeys,
                                                uint32_t* __restrict__ tvals, uint32_t* __restrict__ counts,
                                                uint64_t* __restrict__ lb, uint32_t* __restrict__ ctr,
-                                               int smem_bins) {
+                                               int smem_bins, int vshift) {
   // Per-tile counts: a shared-memory histogram over the tiles of the block's
   // first view (a depth-sorted block almost always lies in one view), flushed
   // with one global atomic per non-empty bin; other views go straight to
@@ -794,7 +812,7 @@ __global__ void __launch_bounds__(256) k3_emit(const uint64_t* __restrict__ dkey
   if (tid == 0) {
     const uint32_t b = atomicAdd(ctr, 1u);
     s_bid = b;
-    s_view0 = (uint32_t)(dkeys[(int64_t)b * K3_TILE] >> 32);
+    s_view0 = (uint32_t)(dkeys[(int64_t)b * K3_TILE] >> vshift);
   }
   for (int t = tid; t < smem_bins; t += 256) s_cnt[t] = 0;
   __syncthreads();
@@ -813,9 +831,9 @@ __global__ void __launch_bounds__(256) k3_emit(const uint64_t* __restrict__ dkey
     g[r] = 0;
     view[r] = 0;
     if (e < nvis) {
-      const uint64_t key = dkeys[e];
+      const KeyT key = dkeys[e];
       g[r] = dvals[e];
-      view[r] = (uint32_t)(key >> 32);
+      view[r] = (uint32_t)(key >> vshift);
       const int64_t pi = (int64_t)view[r] * n + g[r];
       s0[r] = __ldg(span + 2 * pi);
       s1[r] = __ldg(span + 2 * pi + 1);
@@ -1011,9 +1029,10 @@ struct OrderSeg {
 __global__ void __launch_bounds__(256) k2c_compact(const OrderSeg* __restrict__ segs, int n_seg,
                                                    const uint32_t* __restrict__ cache,
                                                    const uint32_t* __restrict__ nt_plane, int64_t M, int64_t n,
-                                                   uint64_t* __restrict__ dkeys, uint32_t* __restrict__ dvals,
+                                                   uint32_t* __restrict__ dkeys, uint32_t* __restrict__ dvals,
                                                    uint64_t* __restrict__ lb_vis, uint64_t* __restrict__ lb_k,
-                                                   uint32_t* __restrict__ ctr, uint64_t* __restrict__ totals) {
+                                                   uint32_t* __restrict__ ctr, uint64_t* __restrict__ totals,
+                                                   int vshift) {
   __shared__ uint64_t s_wv[8], s_wk[8];
   __shared__ uint64_t s_pv;
   __shared__ uint32_t s_bid;
@@ -1075,7 +1094,7 @@ __global__ void __launch_bounds__(256) k2c_compact(const OrderSeg* __restrict__ 
     const int64_t i = i0 + k;
     if (i >= M) break;
     if (nt[k]) {
-      dkeys[pv] = (uint64_t)(i / n) << 32;
+      dkeys[pv] = (uint32_t)(i / n) << vshift;
       dvals[pv] = gg[k];
       ++pv;
     }
@@ -1279,10 +1298,17 @@ static gsr_status bin_sort_impl(gsr_ctx* ctx, const uint32_t* bin_rec, int64_t n
   const uint32_t* p_nt = bin_rec + 9 * M;
 
   const int vbits = bits_for((uint64_t)n_views);
-  const int dpasses = (32 + vbits + 7) / 8;               // depth sort passes
   const int tbits = bits_for(T);
   const int tpasses = std::max(1, (tbits + 7) / 8);       // tile sort passes
-  if (dpasses > 5 || tpasses > 4) return set_err(ctx, GSR_EINVAL, "gsr_bin_sort: batch too large");
+  if (tpasses > 4) return set_err(ctx, GSR_EINVAL, "gsr_bin_sort: batch too large");
+  // depth keys: 32-bit (view << dshift | depth - dbase) unless they do not fit
+  const int dshift = 32 - std::max(vbits, 1);
+  float zmin = cams[0].znear;
+  for (int c = 1; c < n_views; ++c) zmin = std::min(zmin, cams[c].znear);
+  uint32_t dbase_bits;
+  std::memcpy(&dbase_bits, &zmin, 4);
+  bool wide = ctx->depth_keys64 || vbits > 8;
+  const int cshift = 26;  // cached order: view << 26 (<= 64 views), no depth bits
 
   // ---- K2: compact + totals ----
   void *dka, *dkb, *dva, *dvb, *hs, *lb, *tot, *eo = nullptr;
@@ -1301,25 +1327,36 @@ static gsr_status bin_sort_impl(gsr_ctx* ctx, const uint32_t* bin_rec, int64_t n
   const size_t nb2 = (size_t)((M + K2_TILE - 1) / K2_TILE);
   const size_t lb1 = align_up(2 * std::max<size_t>(nb2, 1) * 8) + 256;
   if ((s = ensure(ctx, S_LOOKBACK, lb1, &lb)) != GSR_OK) return s;
-  if ((s = check_cuda(ctx, cudaMemsetAsync(lb, 0, lb1, st), "memset lb")) != GSR_OK) return s;
-  if ((s = check_cuda(ctx, cudaMemsetAsync(dhist, 0, 8 * 256 * 4, st), "memset hist")) != GSR_OK) return s;
-  if ((s = check_cuda(ctx, cudaMemsetAsync(tot, 0, 64, st), "memset tot")) != GSR_OK) return s;
   uint64_t* lbv = (uint64_t*)lb;
   uint64_t* lbk = lbv + std::max<size_t>(nb2, 1);
   uint32_t* ctr2 = (uint32_t*)((char*)lb + align_up(2 * std::max<size_t>(nb2, 1) * 8));
-  const int sp2 = stage_begin(ctx, GSR_STAGE_COMPACT, st);
-  if (M > 0 && !co)
-    k2_compact<<<(unsigned)nb2, 256, 0, st>>>(p_depth, p_nt, M, n, (uint64_t*)dka, (uint32_t*)dva,
-                                              (uint32_t*)eo, lbv, lbk, ctr2, (uint64_t*)tot, dhist, dpasses);
-  if (M > 0 && co)
-    k2c_compact<<<(unsigned)nb2, 256, 0, st>>>(co->segs, co->n_seg, co->cache, p_nt, M, n, (uint64_t*)dka,
-                                               (uint32_t*)dva, lbv, lbk, ctr2, (uint64_t*)tot);
-  stage_end(ctx, sp2, st);
-  if ((s = check_cuda(ctx, cudaGetLastError(), "k2_compact")) != GSR_OK) return s;
   uint64_t* hp = (uint64_t*)ctx->host_pinned;
-  if ((s = check_cuda(ctx, cudaMemcpyAsync(hp, tot, 16, cudaMemcpyDeviceToHost, st), "readback")) != GSR_OK)
-    return s;
-  if ((s = check_cuda(ctx, cudaStreamSynchronize(st), "sync")) != GSR_OK) return s;
+  int dpasses = 0;
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    dpasses = wide ? (32 + vbits + 7) / 8 : 4;
+    if ((s = check_cuda(ctx, cudaMemsetAsync(lb, 0, lb1, st), "memset lb")) != GSR_OK) return s;
+    if ((s = check_cuda(ctx, cudaMemsetAsync(dhist, 0, 8 * 256 * 4, st), "memset hist")) != GSR_OK) return s;
+    if ((s = check_cuda(ctx, cudaMemsetAsync(tot, 0, 64, st), "memset tot")) != GSR_OK) return s;
+    const int sp2 = stage_begin(ctx, GSR_STAGE_COMPACT, st);
+    if (M > 0 && !co && wide)
+      k2_compact<uint64_t><<<(unsigned)nb2, 256, 0, st>>>(p_depth, p_nt, M, n, (uint64_t*)dka, (uint32_t*)dva,
+                                                          (uint32_t*)eo, lbv, lbk, ctr2, (uint64_t*)tot, dhist,
+                                                          dpasses, 32, 0u);
+    if (M > 0 && !co && !wide)
+      k2_compact<uint32_t><<<(unsigned)nb2, 256, 0, st>>>(p_depth, p_nt, M, n, (uint32_t*)dka, (uint32_t*)dva,
+                                                          (uint32_t*)eo, lbv, lbk, ctr2, (uint64_t*)tot, dhist,
+                                                          dpasses, dshift, dbase_bits);
+    if (M > 0 && co)
+      k2c_compact<<<(unsigned)nb2, 256, 0, st>>>(co->segs, co->n_seg, co->cache, p_nt, M, n, (uint32_t*)dka,
+                                                 (uint32_t*)dva, lbv, lbk, ctr2, (uint64_t*)tot, cshift);
+    stage_end(ctx, sp2, st);
+    if ((s = check_cuda(ctx, cudaGetLastError(), "k2_compact")) != GSR_OK) return s;
+    if ((s = check_cuda(ctx, cudaMemcpyAsync(hp, tot, 24, cudaMemcpyDeviceToHost, st), "readback")) != GSR_OK)
+      return s;
+    if ((s = check_cuda(ctx, cudaStreamSynchronize(st), "sync")) != GSR_OK) return s;
+    if (co || wide || hp[2] == 0) break;
+    wide = true;  // a depth offset did not fit in 32 - vbits bits: redo with 64-bit keys
+  }
   const int64_t nvis = (int64_t)hp[0];
   const int64_t K = (int64_t)hp[1];
   *n_keys = K;
@@ -1328,7 +1365,8 @@ static gsr_status bin_sort_impl(gsr_ctx* ctx, const uint32_t* bin_rec, int64_t n
   // algorithmic bytes: K2 reads n_tiles of every pair and the depth of
   // the visible ones, writes 12 B per visible pair; K1's 48-B render records of
   // the visible pairs are attributed to the projection stage.
-  account(ctx, GSR_STAGE_COMPACT, M > 0 ? 1 : 0, (co ? 8.0 : 4.0) * M + 12.0 * nvis + (co ? 0.0 : 4.0 * nvis));
+  account(ctx, GSR_STAGE_COMPACT, M > 0 ? 1 : 0,
+          (co ? 8.0 : 4.0) * M + (co ? 0.0 : 4.0) * nvis + (wide && !co ? 12.0 : 8.0) * nvis);
   account(ctx, GSR_STAGE_PROJECT, 0, 80.0 * nvis);
   if (K > capacity) return set_err(ctx, GSR_ECAPACITY, "gsr_bin_sort: capacity too small (n_keys = required)");
   if (K >= (1ll << 31)) return set_err(ctx, GSR_EINVAL, "gsr_bin_sort: K >= 2^31 keys in one batch");
@@ -1348,7 +1386,8 @@ static gsr_status bin_sort_impl(gsr_ctx* ctx, const uint32_t* bin_rec, int64_t n
   if ((s = ensure(ctx, S_COUNTS, T * 4, &cnt)) != GSR_OK) return s;
   const int variant = ctx->sort_variant;
   const int kpt32 = ctx->sort_kpt32;
-  const size_t dtile = pass_tile<uint64_t>(variant), ttile = pass_tile<uint32_t>(variant, kpt32);
+  const size_t dtile = wide ? pass_tile<uint64_t>(variant) : pass_tile<uint32_t>(variant, kpt32);
+  const size_t ttile = pass_tile<uint32_t>(variant, kpt32);
   const size_t nbd = (size_t)((nvis + dtile - 1) / dtile);
   const size_t nb3 = (size_t)((nvis + K3_TILE - 1) / K3_TILE);
   const size_t nbt = (size_t)((K + ttile - 1) / ttile);
@@ -1367,32 +1406,44 @@ static gsr_status bin_sort_impl(gsr_ctx* ctx, const uint32_t* bin_rec, int64_t n
   uint32_t* ctrs = (uint32_t*)((char*)lb + o_c);  // [0..4] depth, [5] k3, [6..9] tile
 
   // ---- K4a: depth sort of the visible pairs (skipped in the cached order) ----
-  const uint64_t* ck = (const uint64_t*)dka;
+  const void* ck = dka;
   const uint32_t* cvv = (const uint32_t*)dva;
   if (!co) {
     int spd = stage_begin(ctx, GSR_STAGE_DEPTH_SORT, st);
     scan_hist<<<1, 256, 0, st>>>(dhist, dbase, dpasses);
+    const int kbits = wide ? 32 + vbits : 32;
     for (int p = 0; p < dpasses; ++p) {
-      uint64_t* ko = (p % 2 == 0) ? (uint64_t*)dkb : (uint64_t*)dka;
+      void* ko = (p % 2 == 0) ? dkb : dka;
       uint32_t* vo = (p % 2 == 0) ? (uint32_t*)dvb : (uint32_t*)dva;
       const int sh = 8 * p;
-      cudaError_t e = run_pass<uint64_t, 0>(variant, ctx->num_sms, ck, cvv, ko, vo, (uint32_t)nvis, sh,
-                                            std::min(8, 32 + vbits - sh), dbase + 256 * p,
-                                            lbd + (size_t)p * nbd * 256, ctrs + p, nullptr, nullptr, 0, 0, st);
+      cudaError_t e = wide ? run_pass<uint64_t, 0>(variant, ctx->num_sms, (const uint64_t*)ck, cvv, (uint64_t*)ko, vo,
+                                                   (uint32_t)nvis, sh, std::min(8, kbits - sh), dbase + 256 * p,
+                                                   lbd + (size_t)p * nbd * 256, ctrs + p, nullptr, nullptr, 0, 0, st)
+                           : run_pass<uint32_t, 0>(variant, ctx->num_sms, (const uint32_t*)ck, cvv, (uint32_t*)ko, vo,
+                                                   (uint32_t)nvis, sh, 8, dbase + 256 * p,
+                                                   lbd + (size_t)p * nbd * 256, ctrs + p, nullptr, nullptr, 0, 0, st,
+                                                   kpt32);
       if ((s = check_cuda(ctx, e, "depth sort pass")) != GSR_OK) return s;
       ck = ko;
       cvv = vo;
     }
     stage_end(ctx, spd, st);
-    account(ctx, GSR_STAGE_DEPTH_SORT, 1 + dpasses * pass_launches(variant), 24.0 * dpasses * nvis);
+    account(ctx, GSR_STAGE_DEPTH_SORT, 1 + dpasses * pass_launches(variant), (wide ? 24.0 : 16.0) * dpasses * nvis);
     if ((s = check_cuda(ctx, cudaGetLastError(), "depth sort")) != GSR_OK) return s;
   }
 
   // ---- K3: emission + counts ----
   int sp = stage_begin(ctx, GSR_STAGE_EMIT, st);
   const int bins = tpv <= 12288 ? (int)tpv : 0;  // <= 48 KB of shared memory
-  k3_emit<<<(unsigned)nb3, 256, bins * 4, st>>>(ck, cvv, nvis, p_span, n, gx, (uint32_t)tpv, W, (uint32_t*)tka,
-                                                (uint32_t*)tva, (uint32_t*)cnt, lb3, ctrs + 5, bins);
+  if (wide && !co)
+    k3_emit<uint64_t><<<(unsigned)nb3, 256, bins * 4, st>>>((const uint64_t*)ck, cvv, nvis, p_span, n, gx,
+                                                            (uint32_t)tpv, W, (uint32_t*)tka, (uint32_t*)tva,
+                                                            (uint32_t*)cnt, lb3, ctrs + 5, bins, 32);
+  else
+    k3_emit<uint32_t><<<(unsigned)nb3, 256, bins * 4, st>>>((const uint32_t*)ck, cvv, nvis, p_span, n, gx,
+                                                            (uint32_t)tpv, W, (uint32_t*)tka, (uint32_t*)tva,
+                                                            (uint32_t*)cnt, lb3, ctrs + 5, bins,
+                                                            co ? cshift : dshift);
   stage_end(ctx, sp, st);
   account(ctx, GSR_STAGE_EMIT, 1, 44.0 * nvis + 8.0 * K + 4.0 * T);
   if ((s = check_cuda(ctx, cudaGetLastError(), "k3_emit")) != GSR_OK) return s;

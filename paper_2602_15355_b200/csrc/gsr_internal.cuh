@@ -123,6 +123,7 @@ struct gsr_ctx {
   int sort_kpt32 = 12;        // tile-sort keys per thread (GSR_KPT: 8 or 12)
   int composite_stages = 4;   // K6 ring depth (GSR_STAGES: 4 or 8)
   int composite_pix = 1;      // K6 pixels per consumer lane (GSR_PIX: 1 or 2)
+  bool depth_keys64 = false;  // force the 64-bit depth-sort keys (GSR_DKEY64=1)
   int composite_variant = 6;  // K6: 1 block-sync LDG, 2 TMA bulk/record, 3 TMA gather4, 4 cp.async, 5 warp-independent LDG, 6 = 5 + exact ellipse-box cull (default)
 };
 

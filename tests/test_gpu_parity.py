@@ -113,7 +113,7 @@ def test_capacity_protocol(ctx):
     sc = synth.make_scene(1, n_override=2000, views=2)
     G = to_dev(sc.field)
     rec = torch.empty((2, 2000, 12), device="cuda")
-    binr = torch.empty((4, 2, 2000), dtype=torch.int32, device="cuda")
+    binr = torch.empty(10 * 2 * 2000, dtype=torch.int32, device="cuda")
     gsr.gsr_project(ctx, G, sc.cameras, rec, binr)
     vals = torch.full((10,), 7, dtype=torch.int32, device="cuda")
     ranges = torch.full((2 * 64, 2), 7, dtype=torch.int32, device="cuda")
@@ -129,7 +129,7 @@ def test_invalid_arguments(ctx):
     sc = synth.make_scene(1, n_override=100, views=2)
     G = to_dev(sc.field)
     rec = torch.empty((2, 100, 12), device="cuda")
-    binr = torch.empty((4, 2, 100), dtype=torch.int32, device="cuda")
+    binr = torch.empty(10 * 2 * 100, dtype=torch.int32, device="cuda")
     bad = sc.cameras.copy()
     bad[1]["width"] = 64
     with pytest.raises(gsr.GsrError) as ei:
@@ -206,3 +206,26 @@ def test_sort_pairs_u64_adversarial(ctx, case):
         d = (k >> np.uint64(8)) & np.uint64((1 << 12) - 1)
         o = np.argsort(d, kind="stable")
         assert np.array_equal(kout.cpu().numpy().view(np.uint64), k[o])
+
+
+def test_depth_key_widths(ctx):
+    """The depth sort uses 32-bit keys (view << (32 - vbits) | depth bits -
+    bits(znear)); a depth offset that does not fit falls back to 64-bit keys.
+    Both paths (and the forced 64-bit path, GSR_DKEY64=1) are bit-exact vs
+    the oracle: 64 views leave 26 depth bits (8 binades above znear = 0.2), so
+    Gaussians at depth 60 and 5e3 force the fallback; 4 views leave 30 bits,
+    enough for a Gaussian at depth 1e9."""
+    from tests.helpers import axis_camera, field_from
+    rng = np.random.default_rng(9)
+    n = 300
+    z = np.concatenate([rng.uniform(1.0, 3.0, n - 3), [60.0, 5e3, 1e9]])
+    means = np.stack([rng.uniform(-0.3, 0.3, n) * z, rng.uniform(-0.3, 0.3, n) * z, z], 1)
+    means[-3:, :2] = 0.0
+    scales = np.exp(rng.normal(-2.5, 0.4, (n, 3))) * (z[:, None] / 2.0)
+    fld = field_from(means, scales, rng.normal(size=(n, 4)), rng.uniform(0.3, 0.99, n),
+                     rng.uniform(0, 1, (n, 3)), rng.uniform(0, 1, n))
+    cam = axis_camera(40, 32, 40.0)
+    cams64 = np.repeat(np.asarray(cam).reshape(1), 64)
+    _full_check(ctx, fld, cams64[:4])   # 30 depth bits: everything fits
+    _full_check(ctx, fld.subset(np.arange(n - 1)), cams64)  # 26 depth bits: 60 and 5e3 overflow -> fallback
+    _full_check(ctx, fld.subset(np.arange(n - 3)), cams64)  # fits: 32-bit keys
