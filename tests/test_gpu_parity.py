@@ -229,3 +229,23 @@ def test_depth_key_widths(ctx):
     _full_check(ctx, fld, cams64[:4])   # 30 depth bits: everything fits
     _full_check(ctx, fld.subset(np.arange(n - 1)), cams64)  # 26 depth bits: 60 and 5e3 overflow -> fallback
     _full_check(ctx, fld.subset(np.arange(n - 3)), cams64)  # fits: 32-bit keys
+
+
+@pytest.mark.parametrize("env", ["GSR_COMPOSITE=1", "GSR_COMPOSITE=2", "GSR_COMPOSITE=3", "GSR_COMPOSITE=4",
+                                 "GSR_COMPOSITE=5", "GSR_COMPOSITE=3 GSR_STAGES=8", "GSR_COMPOSITE=3 GSR_PIX=2",
+                                 "GSR_SORT=2", "GSR_SORT=3", "GSR_KPT=8"])
+def test_measured_variants_stay_exact(env, monkeypatch):
+    """Every A/B variant DESIGN.md reports a measurement for (K6 loaders: block-
+    synchronous LDG, TMA bulk per record, TMA tile::gather4, cp.async; the
+    8-stage ring; 2 pixels per lane; warp-independent without the exact cull;
+    sort passes: persistent TMA-fed onesweep, reduce-then-scan; 8 keys per
+    thread) reproduces the oracle bit for bit.  Variants are chosen by
+    environment variables read when a context is created."""
+    from paper_2602_15355_b200 import Context
+    for kv in env.split():
+        k, v = kv.split("=")
+        monkeypatch.setenv(k, v)
+    c = Context(0)
+    fld, cams = synth.random_scene_small(11, 900, 100, 37, 90.0, 3, 2, logscale_mu=-2.6)
+    g, o = _full_check(c, fld, cams)
+    assert np.array_equal(g["rgbu"], o["rgbu"])
