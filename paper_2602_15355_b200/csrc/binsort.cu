@@ -984,6 +984,174 @@ __global__ void __launch_bounds__(1024) k5_ranges(const uint32_t* __restrict__ c
   }
 }
 
+// ---------------------------------------------------------------------------
+// K4c: the tile sort as a stable counting scatter (default; the two onesweep
+// passes of K4b remain for tiles-per-view > CS_MAX_TPV).  The duplicated keys
+// are view-major (K3 emits view by view), every tile's output range is known
+// from K5, so only each key's rank among the earlier keys of its tile is
+// needed.  Chunks of CS_CHUNK keys never straddle a view:
+//   cs_hist  per chunk, per tile of the chunk's view: key counts -> H[chunk][tpv]
+//   cs_scan  per (view, tile): H[chunk][tile] <- ranges[tile].start + counts of
+//            the view's earlier chunks (column scan, in place)
+//   cs_scatter per chunk, in sub-rounds of W x 32 x CS_KPT keys: warp-local
+//            stable ranks (ballot match on the tile digit), exclusive prefix
+//            over the warps, plus the chunk's running per-tile counter; the
+//            value goes straight to its final slot.
+// DRAM traffic per key: 4 B (hist) + 8 B read + 4 B write (scatter) + the
+// H matrix (CS_CHUNK = 16 K keys: ~1 B/key), vs 28 B/key for two passes.
+constexpr int CS_KPT = 16;
+constexpr int CS_CHUNK = 16384;
+constexpr int CS_MAX_TPV = 12288;
+
+// view / chunk bookkeeping (K5 tail): vs[v] = first key of view v (vs[V] = K),
+// pb[v] = first chunk of view v (pb[V] = chunks)
+__device__ __forceinline__ void cs_locate(const uint32_t* __restrict__ meta, int V, uint32_t chunk, int& v,
+                                          uint32_t& k0, uint32_t& k1) {
+  const uint32_t* vs = meta;
+  const uint32_t* pb = meta + (V + 1);
+  int lo = 0, hi = V - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (pb[mid] <= chunk) lo = mid; else hi = mid - 1;
+  }
+  v = lo;
+  k0 = vs[v] + (chunk - pb[v]) * (uint32_t)CS_CHUNK;
+  k1 = min(k0 + (uint32_t)CS_CHUNK, vs[v + 1]);
+}
+
+__global__ void __launch_bounds__(256) cs_meta(const uint2* __restrict__ ranges, int V, uint32_t tpv, uint32_t K,
+                                               uint32_t* __restrict__ meta) {
+  if (threadIdx.x != 0) return;
+  uint32_t pb = 0;
+  for (int v = 0; v <= V; ++v) {
+    const uint32_t s = v < V ? ranges[(size_t)v * tpv].x : K;
+    meta[v] = s;
+    meta[(V + 1) + v] = pb;
+    if (v < V) {
+      const uint32_t e = (v + 1 < V) ? ranges[(size_t)(v + 1) * tpv].x : K;
+      pb += (e - s + CS_CHUNK - 1) / CS_CHUNK;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) cs_hist(const uint32_t* __restrict__ tkeys, const uint32_t* __restrict__ meta,
+                                               int V, uint32_t tpv, uint32_t* __restrict__ H) {
+  extern __shared__ uint32_t s_h[];
+  const uint32_t chunk = blockIdx.x;
+  if (chunk >= meta[(V + 1) + V]) return;
+  int v;
+  uint32_t k0, k1;
+  cs_locate(meta, V, chunk, v, k0, k1);
+  for (uint32_t d = threadIdx.x; d < tpv; d += 256) s_h[d] = 0;
+  __syncthreads();
+  const uint32_t vb = (uint32_t)v * tpv;
+  for (uint32_t i = k0 + threadIdx.x; i < k1; i += 256) atomicAdd(s_h + (__ldg(tkeys + i) - vb), 1u);
+  __syncthreads();
+  uint32_t* row = H + (size_t)chunk * tpv;
+  for (uint32_t d = threadIdx.x; d < tpv; d += 256) row[d] = s_h[d];
+}
+
+__global__ void __launch_bounds__(256) cs_scan(const uint2* __restrict__ ranges, const uint32_t* __restrict__ meta,
+                                               int V, uint32_t tpv, uint32_t* __restrict__ H) {
+  const uint64_t t = (uint64_t)blockIdx.x * 256 + threadIdx.x;  // global tile = v * tpv + d
+  if (t >= (uint64_t)V * tpv) return;
+  const int v = (int)(t / tpv);
+  const uint32_t d = (uint32_t)(t - (uint64_t)v * tpv);
+  const uint32_t* pb = meta + (V + 1);
+  uint32_t run = ranges[t].x;
+  for (uint32_t c = pb[v]; c < pb[v + 1]; ++c) {
+    uint32_t* p = H + (size_t)c * tpv + d;
+    const uint32_t x = *p;
+    *p = run;
+    run += x;
+  }
+}
+
+template <int W>
+__global__ void __launch_bounds__(W * 32) cs_scatter(const uint32_t* __restrict__ tkeys,
+                                                     const uint32_t* __restrict__ tvals,
+                                                     const uint32_t* __restrict__ meta, int V, uint32_t tpv,
+                                                     int dbits, const uint32_t* __restrict__ H,
+                                                     uint32_t* __restrict__ vals_out, uint64_t* __restrict__ keys64,
+                                                     const uint32_t* __restrict__ depth_plane, int64_t nper) {
+  // shared memory: s_base [tpv] u32 (chunk offset + keys so far), s_sub [tpv]
+  // u32 (this sub-round's base), s_wh [W][tpv] u16 (per-warp counts, then
+  // the exclusive prefix over the warps)
+  extern __shared__ uint32_t smem[];
+  uint32_t* s_base = smem;
+  uint32_t* s_sub = smem + tpv;
+  uint16_t* s_wh = reinterpret_cast<uint16_t*>(smem + 2 * tpv);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t chunk = blockIdx.x;
+  if (chunk >= meta[(V + 1) + V]) return;
+  int v;
+  uint32_t k0, k1;
+  cs_locate(meta, V, chunk, v, k0, k1);
+  const uint32_t vb = (uint32_t)v * tpv;
+  const uint32_t* Hrow = H + (size_t)chunk * tpv;
+  for (uint32_t d = tid; d < tpv; d += W * 32) s_base[d] = Hrow[d];
+  for (uint32_t i = tid; i < (uint32_t)W * tpv; i += W * 32) s_wh[i] = 0;
+  __syncthreads();
+  const uint32_t lt = (1u << lane) - 1u;
+  uint16_t* wh = s_wh + (size_t)warp * tpv;
+  constexpr uint32_t SUB = W * 32 * CS_KPT;
+  for (uint32_t s0 = k0; s0 < k1; s0 += SUB) {
+    const uint32_t wb = s0 + (uint32_t)warp * (32 * CS_KPT);
+    uint32_t dg[CS_KPT], vv[CS_KPT], rk[CS_KPT];
+#pragma unroll
+    for (int k = 0; k < CS_KPT; ++k) {
+      const uint32_t i = wb + k * 32 + lane;
+      const bool ok = i < k1;
+      dg[k] = ok ? __ldg(tkeys + i) - vb : 0u;
+      vv[k] = ok ? __ldg(tvals + i) : 0u;
+    }
+    // warp-local stable ranks: lanes holding the same tile digit (ballots per bit)
+#pragma unroll
+    for (int k = 0; k < CS_KPT; ++k) {
+      const uint32_t i = wb + k * 32 + lane;
+      const bool ok = i < k1;
+      uint32_t peers = __ballot_sync(FULL, ok);
+      for (int b = 0; b < dbits; ++b) {
+        const bool bit = (dg[k] >> b) & 1u;
+        const uint32_t bb = __ballot_sync(FULL, bit);
+        peers &= bit ? bb : ~bb;
+      }
+      uint32_t pre = 0;
+      if (ok) pre = wh[dg[k]];
+      __syncwarp();
+      if (ok && (peers & lt) == 0) wh[dg[k]] = (uint16_t)(pre + __popc(peers));
+      __syncwarp();
+      rk[k] = pre + __popc(peers & lt);
+    }
+    __syncthreads();
+    for (uint32_t d = tid; d < tpv; d += W * 32) {
+      uint32_t run = 0;
+#pragma unroll
+      for (int w = 0; w < W; ++w) {
+        const uint32_t c = s_wh[(size_t)w * tpv + d];
+        s_wh[(size_t)w * tpv + d] = (uint16_t)run;
+        run += c;
+      }
+      const uint32_t b = s_base[d];
+      s_sub[d] = b;
+      s_base[d] = b + run;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < CS_KPT; ++k) {
+      const uint32_t i = wb + k * 32 + lane;
+      if (i < k1) {
+        const uint32_t pos = s_sub[dg[k]] + (uint32_t)wh[dg[k]] + rk[k];
+        vals_out[pos] = vv[k];
+        if (keys64) keys64[pos] = ((uint64_t)(vb + dg[k]) << 32) | __ldg(depth_plane + (int64_t)v * nper + vv[k]);
+      }
+    }
+    __syncthreads();
+    for (uint32_t i = tid; i < (uint32_t)W * tpv; i += W * 32) s_wh[i] = 0;
+    __syncthreads();
+  }
+}
+
 // O2 emission order (view, g, ty, tx): parity output only.
 __global__ void __launch_bounds__(256) k_emit_o2(const uint32_t* __restrict__ depth_plane,
                                                  const uint4* __restrict__ span,
@@ -1455,7 +1623,41 @@ static gsr_status bin_sort_impl(gsr_ctx* ctx, const uint32_t* bin_rec, int64_t n
   account(ctx, GSR_STAGE_RANGES, 1, 12.0 * T);
   if ((s = check_cuda(ctx, cudaGetLastError(), "k5_ranges")) != GSR_OK) return s;
 
-  // ---- K4b: tile sort ----
+  // ---- K4b / K4c: tile sort ----
+  if (tpv <= (uint64_t)CS_MAX_TPV && !ctx->tile_sort_radix) {
+    // K4c counting scatter (default)
+    const uint64_t nchunks_max = (uint64_t)(K + CS_CHUNK - 1) / CS_CHUNK + (uint64_t)n_views;
+    void *hm, *meta;
+    if ((s = ensure(ctx, S_CSH, nchunks_max * tpv * 4, &hm)) != GSR_OK) return s;
+    if ((s = ensure(ctx, S_CSMETA, 2 * (n_views + 1) * 4, &meta)) != GSR_OK) return s;
+    const int W = (24 * tpv <= 100 * 1024) ? 8 : 4;
+    const size_t smem = (size_t)tpv * (8 + 2 * W);
+    sp = stage_begin(ctx, GSR_STAGE_TILE_SORT, st);
+    cs_meta<<<1, 32, 0, st>>>((const uint2*)ranges, n_views, (uint32_t)tpv, (uint32_t)K, (uint32_t*)meta);
+    cs_hist<<<(unsigned)nchunks_max, 256, tpv * 4, st>>>((const uint32_t*)tka, (const uint32_t*)meta, n_views,
+                                                          (uint32_t)tpv, (uint32_t*)hm);
+    cs_scan<<<(unsigned)((T + 255) / 256), 256, 0, st>>>((const uint2*)ranges, (const uint32_t*)meta, n_views,
+                                                         (uint32_t)tpv, (uint32_t*)hm);
+    const int dbits = std::max(1, bits_for(tpv));
+    if (W == 8) {
+      cudaFuncSetAttribute(cs_scatter<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cs_scatter<8><<<(unsigned)nchunks_max, 256, smem, st>>>((const uint32_t*)tka, (const uint32_t*)tva,
+                                                              (const uint32_t*)meta, n_views, (uint32_t)tpv, dbits,
+                                                              (const uint32_t*)hm, vals, keys, p_depth, n);
+    } else {
+      cudaFuncSetAttribute(cs_scatter<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cs_scatter<4><<<(unsigned)nchunks_max, 128, smem, st>>>((const uint32_t*)tka, (const uint32_t*)tva,
+                                                              (const uint32_t*)meta, n_views, (uint32_t)tpv, dbits,
+                                                              (const uint32_t*)hm, vals, keys, p_depth, n);
+    }
+    stage_end(ctx, sp, st);
+    // hist reads 4 B/key; scatter reads 8 B/key and writes the 4-B values
+    // (+ 8-B keys when asked); the chunk x tile matrix is written, scanned in
+    // place and read once
+    const double hbytes = (double)(K + CS_CHUNK - 1) / CS_CHUNK * (double)tpv * 4.0;
+    account(ctx, GSR_STAGE_TILE_SORT, 4, (16.0 + (keys ? 8.0 : 0.0)) * K + 4.0 * hbytes);
+    if ((s = check_cuda(ctx, cudaGetLastError(), "tile counting scatter")) != GSR_OK) return s;
+  } else {
   sp = stage_begin(ctx, GSR_STAGE_TILE_SORT, st);
   const uint32_t* tk = (const uint32_t*)tka;
   const uint32_t* tv = (const uint32_t*)tva;
@@ -1483,6 +1685,8 @@ static gsr_status bin_sort_impl(gsr_ctx* ctx, const uint32_t* bin_rec, int64_t n
   account(ctx, GSR_STAGE_TILE_SORT, tpasses * pass_launches(variant),
           16.0 * (tpasses - 1) * K + (12.0 + (keys ? 8.0 : 0.0)) * K);
   if ((s = check_cuda(ctx, cudaGetLastError(), "tile sort")) != GSR_OK) return s;
+
+  }
 
   // ---- optional O2 emission-order list ----
   if (keys_unsorted) {
