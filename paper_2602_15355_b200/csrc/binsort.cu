@@ -1059,7 +1059,20 @@ __global__ void __launch_bounds__(256) cs_scan(const uint2* __restrict__ ranges,
   const uint32_t d = (uint32_t)(t - (uint64_t)v * tpv);
   const uint32_t* pb = meta + (V + 1);
   uint32_t run = ranges[t].x;
-  for (uint32_t c = pb[v]; c < pb[v + 1]; ++c) {
+  const uint32_t c1 = pb[v + 1];
+  uint32_t c = pb[v];
+  // 8 independent loads in flight per step (the column walk is latency-bound)
+  for (; c + 8 <= c1; c += 8) {
+    uint32_t x[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) x[j] = H[(size_t)(c + j) * tpv + d];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      H[(size_t)(c + j) * tpv + d] = run;
+      run += x[j];
+    }
+  }
+  for (; c < c1; ++c) {
     uint32_t* p = H + (size_t)c * tpv + d;
     const uint32_t x = *p;
     *p = run;
