@@ -999,7 +999,7 @@ __global__ void __launch_bounds__(1024) k5_ranges(const uint32_t* __restrict__ c
 //            value goes straight to its final slot.
 // DRAM traffic per key: 4 B (hist) + 8 B read + 4 B write (scatter) + the
 // H matrix (CS_CHUNK = 16 K keys: ~1 B/key), vs 28 B/key for two passes.
-constexpr int CS_KPT = 16;
+constexpr int CS_KPT = 8;
 constexpr int CS_CHUNK = 16384;
 constexpr int CS_MAX_TPV = 12288;
 
