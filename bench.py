@@ -414,7 +414,7 @@ def main():
     # Rooflines: the dominant kernel of the step is
     # K6 (composite), bound by FP32/ALU issue; its algorithmic work is SURVEY
     # §8(d)'s 28 ops per evaluated (pixel, entry) pair of the plain definition +
-    # 8 per blended fragment.  The key sort (K4b tile sort) is reported against
+    # 8 per blended fragment.  The key sort (K4c tile sort) is reported against
     # HBM, as the north_star asks.  Both use device times from CUDA events
     # bracketing those kernels on their launch stream inside the timed region.
     f_clk = (clk.get("sm_mhz") or peaks["sm_max_mhz"]) * 1e6
@@ -433,7 +433,8 @@ def main():
             "share_of_step": round(st_ms["composite"] / sum(st_ms.values()), 3),
             "launches_per_step": n_comp}
     ach_sort = st_by["tile_sort"] / (st_ms["tile_sort"] / 1e3) / 1e9
-    roof_sort = {"bound": "hbm", "kernel": "tile_sort (K4b onesweep passes)", "achieved": round(ach_sort, 1),
+    roof_sort = {"bound": "hbm", "kernel": "tile_sort (K4c counting scatter: chunk histograms + column scan + "
+                                            "ranked scatter)", "achieved": round(ach_sort, 1),
                  "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": round(ach_sort / peaks["hbm_gbs"], 4),
                  "traffic": traffic.get("tile_sort"),
                  "peak_source": peaks["source"] + " hbm_gbs (MEASURED_PEAKS.json)",
