@@ -295,6 +295,40 @@ def bench_backward(G, dev, reps: int = 3):
             "config": "c3 field (1M Gaussians, SH 3), 16 views 800x800, L2 loss vs a perturbed image"}
 
 
+def bench_hierarchical(dev, reps: int = 2):
+    """configs[4] (hierarchical coarse-to-fine scoring, PAPER.md L5 / Alg. 1
+    top-k): 2 M Gaussians; coarse pass over 4,096 candidates at 256x256
+    (f = 288), top-64 by (score desc, index asc), fine pass re-rendering those
+    64 at 1024x1024 (f = 1152), NBV = fine argmax.  One GPU (the all-gather
+    between the passes is the N > 1 plumbing of distributed.hierarchical_select)."""
+    import torch
+    import synth
+    from paper_2602_15355_b200 import Gaussians
+    from paper_2602_15355_b200.distributed import hierarchical_select
+    from paper_2602_15355_b200.pipeline import ViewScorer
+    sc = synth.make_scene(5)
+    G = Gaussians(torch.from_numpy(sc.field.planes).to(dev), sc.field.sh_degree)
+    coarse = ViewScorer(G, batch_views=64, n_slots=2)
+    fine = ViewScorer(G, batch_views=16, n_slots=2)
+
+    def run():
+        return hierarchical_select(sc.cameras, lambda c: synth.with_resolution(c, 1024, 1024, 1152.0),
+                                   coarse.score_views, fine.score_views,
+                                   lambda s, k, ex: coarse.select(s, k, ex), top_k=64)
+    run()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        cs, top, fs, nbv = run()
+    e1.record()
+    torch.cuda.synchronize()
+    t = e0.elapsed_time(e1) / reps / 1e3
+    return {"metric": "hierarchical_passes_per_sec", "value": round(1.0 / t, 2), "unit": "passes/s",
+            "ms_per_pass": round(t * 1e3, 2), "candidate_views_per_sec": round((4096 + 64) / t, 1),
+            "nbv": int(nbv), "config": "c5: 2M Gaussians, 4096 coarse views 256^2 -> top-64 fine 1024^2"}
+
+
 # ----------------------------------------------------------------------------- GPU arm
 def main():
     args = parse()
@@ -454,6 +488,7 @@ def main():
         line["next4_sobel"] = bench_sobel(gsr, dev, peaks)
         line["next3_backward"] = bench_backward(G, dev)
         line["next2_wang"] = bench_wang(dev)
+        line["c5_hierarchical"] = bench_hierarchical(dev)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(scene, args.cpu_views)
     if rank == 0:
