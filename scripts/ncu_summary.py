@@ -64,7 +64,7 @@ def ncu_raw(rep):
         "warp_inst": "smsp__inst_executed.sum",
     }
     scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-6, "usecond": 1e-3,
-             "msecond": 1.0, "second": 1e3}
+             "msecond": 1.0, "second": 1e3, "ns": 1e-6, "us": 1e-3, "ms": 1.0, "s": 1e3}
     res = []
     for r in data:
         d = {"kernel": short(r[hdr.index("Kernel Name")])}
