@@ -1000,7 +1000,7 @@ __global__ void __launch_bounds__(1024) k5_ranges(const uint32_t* __restrict__ c
 // DRAM traffic per key: 4 B (hist) + 8 B read + 4 B write (scatter) + the
 // H matrix (CS_CHUNK = 16 K keys: ~1 B/key), vs 28 B/key for two passes.
 constexpr int CS_KPT = 8;
-constexpr int CS_CHUNK = 16384;
+constexpr int CS_CHUNK = 32768;
 constexpr int CS_MAX_TPV = 12288;
 
 // view / chunk bookkeeping (K5 tail): vs[v] = first key of view v (vs[V] = K),
@@ -1061,13 +1061,13 @@ __global__ void __launch_bounds__(256) cs_scan(const uint2* __restrict__ ranges,
   uint32_t run = ranges[t].x;
   const uint32_t c1 = pb[v + 1];
   uint32_t c = pb[v];
-  // 8 independent loads in flight per step (the column walk is latency-bound)
-  for (; c + 8 <= c1; c += 8) {
-    uint32_t x[8];
+  // 16 independent loads in flight per step (the column walk is latency-bound)
+  for (; c + 16 <= c1; c += 16) {
+    uint32_t x[16];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) x[j] = H[(size_t)(c + j) * tpv + d];
+    for (int j = 0; j < 16; ++j) x[j] = H[(size_t)(c + j) * tpv + d];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
+    for (int j = 0; j < 16; ++j) {
       H[(size_t)(c + j) * tpv + d] = run;
       run += x[j];
     }
