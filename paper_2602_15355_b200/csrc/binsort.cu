@@ -1090,10 +1090,13 @@ __global__ void __launch_bounds__(W * 32) cs_scatter(const uint32_t* __restrict_
   // shared memory: s_base [tpv] u32 (chunk offset + keys so far), s_sub [tpv]
   // u32 (this sub-round's base), s_wh [W][tpv] u16 (per-warp counts, then
   // the exclusive prefix over the warps)
+  // per-warp rows are padded to a multiple of 8 tiles (16 B) so the prefix
+  // loop can work on packed u16 pairs and the reset on 16-byte stores
   extern __shared__ uint32_t smem[];
+  const uint32_t ts = (tpv + 7u) & ~7u;  // row stride (u16 elements)
   uint32_t* s_base = smem;
-  uint32_t* s_sub = smem + tpv;
-  uint16_t* s_wh = reinterpret_cast<uint16_t*>(smem + 2 * tpv);
+  uint32_t* s_sub = smem + ts;
+  uint16_t* s_wh = reinterpret_cast<uint16_t*>(smem + 2 * ts);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t chunk = blockIdx.x;
   if (chunk >= meta[(V + 1) + V]) return;
@@ -1103,10 +1106,10 @@ __global__ void __launch_bounds__(W * 32) cs_scatter(const uint32_t* __restrict_
   const uint32_t vb = (uint32_t)v * tpv;
   const uint32_t* Hrow = H + (size_t)chunk * tpv;
   for (uint32_t d = tid; d < tpv; d += W * 32) s_base[d] = Hrow[d];
-  for (uint32_t i = tid; i < (uint32_t)W * tpv; i += W * 32) s_wh[i] = 0;
+  for (uint32_t i = tid; i < (uint32_t)W * ts / 8; i += W * 32) reinterpret_cast<uint4*>(s_wh)[i] = make_uint4(0, 0, 0, 0);
   __syncthreads();
   const uint32_t lt = (1u << lane) - 1u;
-  uint16_t* wh = s_wh + (size_t)warp * tpv;
+  uint16_t* wh = s_wh + (size_t)warp * ts;
   constexpr uint32_t SUB = W * 32 * CS_KPT;
   for (uint32_t s0 = k0; s0 < k1; s0 += SUB) {
     const uint32_t wb = s0 + (uint32_t)warp * (32 * CS_KPT);
@@ -1137,17 +1140,29 @@ __global__ void __launch_bounds__(W * 32) cs_scatter(const uint32_t* __restrict_
       rk[k] = pre + __popc(peers & lt);
     }
     __syncthreads();
-    for (uint32_t d = tid; d < tpv; d += W * 32) {
+    // exclusive prefix over the warps, two tiles per 32-bit word (no carry:
+    // a sub-round holds at most W x 32 x CS_KPT < 2^16 keys)
+    const uint32_t* wh32 = reinterpret_cast<const uint32_t*>(s_wh);
+    for (uint32_t p = tid; p < ts / 2; p += W * 32) {
       uint32_t run = 0;
 #pragma unroll
       for (int w = 0; w < W; ++w) {
-        const uint32_t c = s_wh[(size_t)w * tpv + d];
-        s_wh[(size_t)w * tpv + d] = (uint16_t)run;
+        uint32_t* q = const_cast<uint32_t*>(wh32) + (size_t)w * (ts / 2) + p;
+        const uint32_t c = *q;
+        *q = run;
         run += c;
       }
-      const uint32_t b = s_base[d];
-      s_sub[d] = b;
-      s_base[d] = b + run;
+      const uint32_t d = 2 * p;
+      if (d < tpv) {
+        const uint32_t b = s_base[d];
+        s_sub[d] = b;
+        s_base[d] = b + (run & 0xffffu);
+      }
+      if (d + 1 < tpv) {
+        const uint32_t b = s_base[d + 1];
+        s_sub[d + 1] = b;
+        s_base[d + 1] = b + (run >> 16);
+      }
     }
     __syncthreads();
 #pragma unroll
@@ -1160,7 +1175,7 @@ __global__ void __launch_bounds__(W * 32) cs_scatter(const uint32_t* __restrict_
       }
     }
     __syncthreads();
-    for (uint32_t i = tid; i < (uint32_t)W * tpv; i += W * 32) s_wh[i] = 0;
+    for (uint32_t i = tid; i < (uint32_t)W * ts / 8; i += W * 32) reinterpret_cast<uint4*>(s_wh)[i] = make_uint4(0, 0, 0, 0);
     __syncthreads();
   }
 }
@@ -1644,7 +1659,7 @@ static gsr_status bin_sort_impl(gsr_ctx* ctx, const uint32_t* bin_rec, int64_t n
     if ((s = ensure(ctx, S_CSH, nchunks_max * tpv * 4, &hm)) != GSR_OK) return s;
     if ((s = ensure(ctx, S_CSMETA, 2 * (n_views + 1) * 4, &meta)) != GSR_OK) return s;
     const int W = (24 * tpv <= 100 * 1024) ? 8 : 4;
-    const size_t smem = (size_t)tpv * (8 + 2 * W);
+    const size_t smem = (size_t)((tpv + 7) & ~7ull) * (8 + 2 * W);
     sp = stage_begin(ctx, GSR_STAGE_TILE_SORT, st);
     cs_meta<<<1, 32, 0, st>>>((const uint2*)ranges, n_views, (uint32_t)tpv, (uint32_t)K, (uint32_t*)meta);
     cs_hist<<<(unsigned)nchunks_max, 256, tpv * 4, st>>>((const uint32_t*)tka, (const uint32_t*)meta, n_views,
