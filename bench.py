@@ -474,12 +474,37 @@ def main():
                  "peak_source": peaks["source"] + " hbm_gbs (MEASURED_PEAKS.json)",
                  "share_of_step": round(st_ms["tile_sort"] / sum(st_ms.values()), 3)}
 
+    # the same K6 roofline with K6 alone on the GPU (one slot, one step): the
+    # two-stream spans above include time the composite shares with the sorts
+    iso = None
+    if not args.no_extras and world == 1:
+        iso_scorer = ViewScorer(G, batch_views=args.batch_views, n_slots=1)
+        iso_scorer.score_views(cams)
+        iso_scorer.timing(True)
+        iso_scorer.timing_read()
+        iso_scorer.reset_counters()
+        torch.cuda.synchronize()
+        iso_scorer.score_views(cams)
+        torch.cuda.synchronize()
+        ist = iso_scorer.timing_read()
+        ifr = iso_scorer.n_frag.to(torch.float64).tolist()
+        it = ist["composite"]["ms"] / 1e3
+        iso_ops = (28.0 * ifr[1] + 8.0 * ifr[0]) / it / 1e12
+        iso = {"bound": "alu", "kernel": "k6_composite (one stream)", "achieved": round(iso_ops, 2),
+               "peak": round(peak_ops, 2), "unit": "Top/s", "frac": round(iso_ops / peak_ops, 4),
+               "ms_per_step": round(ist["composite"]["ms"], 2),
+               "share_of_serial_step": round(ist["composite"]["ms"] / sum(v["ms"] for v in ist.values()), 3)}
+        iso_scorer.timing(False)
+        del iso_scorer
+        torch.cuda.empty_cache()
+
     line = {"metric": METRIC, "value": round(views_per_s, 2), "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 3),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (seeded generator of BASELINE.json configs[2]; no dataset)",
             "config": cfg_json, "fragments_per_sec": frag_per_s, "evaluated_pairs_per_sec": eval_per_s,
-            "wall_ms_per_step": round(wall_ms / args.steps, 3), "roofline": roof, "roofline_sort": roof_sort,
+            "wall_ms_per_step": round(wall_ms / args.steps, 3), "roofline": roof, "roofline_isolated": iso,
+            "roofline_sort": roof_sort,
             "stages": stage_tab,
             "gpu_launches": int(launches * world), "clocks": clk, "e2e": e2e,
             "keys_per_step_rank0": int(sum(scorer.last_keys))}
