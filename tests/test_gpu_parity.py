@@ -250,3 +250,47 @@ def test_measured_variants_stay_exact(env, monkeypatch):
     fld, cams = synth.random_scene_small(11, 900, 100, 37, 90.0, 3, 2, logscale_mu=-2.6)
     g, o = _full_check(c, fld, cams)
     assert np.array_equal(g["rgbu"], o["rgbu"])
+
+
+def test_empty_field_and_huge_gaussian(ctx):
+    """n = 0 (empty field) scores 0 through ViewScorer; one Gaussian larger
+    than the image (every tile, many rows / long spans in K1 and K3) plus small
+    ones in front of and behind it: bit-exact vs the oracle."""
+    from paper_2602_15355_b200.pipeline import ViewScorer
+    from tests.helpers import axis_camera, field_from
+    empty = synth.GaussianField(np.zeros((3, 0, 4), np.float32), 0)
+    cam = axis_camera(70, 45, 60.0)
+    cams = np.repeat(np.asarray(cam).reshape(1), 2)
+    from paper_2602_15355_b200 import Gaussians
+    G0 = Gaussians(torch.zeros((3, 0, 4), device="cuda"), 0)
+    s = ViewScorer(G0, batch_views=2).score_views(cams)
+    assert s.shape == (2,) and torch.all(s == 0)
+    rng = np.random.default_rng(12)
+    n = 40
+    means = np.concatenate([[[0.0, 0.0, 2.0]], np.stack([rng.uniform(-0.5, 0.5, n - 1), rng.uniform(-0.4, 0.4, n - 1),
+                                                          rng.uniform(1.0, 3.0, n - 1)], 1)])
+    scales = np.concatenate([[[3.0, 2.0, 0.5]], np.exp(rng.normal(-3.0, 0.4, (n - 1, 3)))])
+    fld = field_from(means, scales, rng.normal(size=(n, 4)), np.r_[0.6, rng.uniform(0.3, 0.9, n - 1)],
+                     rng.uniform(0, 1, (n, 3)), rng.uniform(0, 1, n))
+    g, o = _full_check(ctx, fld, cams)
+    assert np.array_equal(g["rgbu"], o["rgbu"])
+    assert o["projs"][0]["n_tiles"][0] == 5 * 3  # the big one covers every tile of the 70x45 image
+
+
+def test_invalid_next_arguments(ctx):
+    """EINVAL for the NEXT entry points' bad arguments: LOD levels / delta /
+    thresholds, cache tile ranges that do not cover the field, Sobel on images
+    smaller than the kernel."""
+    from paper_2602_15355_b200 import Lod, gsr
+    sc = synth.make_scene(1, n_override=64, views=2)
+    G = to_dev(sc.field)
+    rec = torch.empty((2, 64, 12), device="cuda")
+    binr = torch.empty(10 * 2 * 64, dtype=torch.int32, device="cuda")
+    tl = torch.zeros((64, 4), device="cuda")
+    for levels, delta, th in [(0, 0.3, [1.0]), (3, 0.0, [1.0, 2.0]), (3, 0.3, [2.0, 1.0]), (9, 0.3, [1.0] * 7)]:
+        with pytest.raises(gsr.GsrError) as ei:
+            gsr.gsr_project(ctx, G, sc.cameras, rec, binr, lod=Lod(tl, levels, delta, th))
+        assert ei.value.status == gsr.GSR_EINVAL
+    with pytest.raises(gsr.GsrError) as ei:
+        gsr.OrderCache(ctx, G, [0, 30], [8], [[0.0, 0.0, 0.0]])  # does not cover [0, 64)
+    assert ei.value.status == gsr.GSR_EINVAL
