@@ -274,6 +274,24 @@ gsr_status gsr_backward(gsr_ctx* ctx, const gsr_gaussians* gaussians, const gsr_
                         const uint32_t* vals, const uint32_t* ranges, const float* rgbu,
                         const float* dl_drgbu, float* grads, void* stream);
 
+/* ---- NEXT-3: refinement step of UPDATE_GS ("bounded refinement (5k
+   iterations per inserted image)", §4.1) ----------------------
+   gsr_l2_loss: L = (1/N) sum_p sum_ch w_ch (img - target)^2 over N = n_pixels
+     (r, g, b, U) pixels; dl_dimg OPTIONAL receives dL/dimg = (2/N) w (img -
+     target) (the upstream gradient of gsr_backward); loss [device, 1 double].
+     weights [host] 4 floats.
+   gsr_adam_step: Adam (Kingma & Ba 2015, bias-corrected, step >= 1) on the
+     field planes params [planes][n][4] with grads, moments m, v of the same
+     layout, a learning rate per (plane, component) lr [host] [planes][4];
+     afterwards opacity is clamped to [1e-4, 1], scales to >= 1e-6 and the
+     uncertainty to >= 0 (projection onto the activated parameters' domain).
+   Pruning and densification are out of scope. */
+gsr_status gsr_l2_loss(gsr_ctx* ctx, const float* img, const float* target, int64_t n_pixels, const float* weights,
+                       float* dl_dimg, double* loss, void* stream);
+gsr_status gsr_adam_step(gsr_ctx* ctx, float* params, const float* grads, float* m, float* v, int64_t n,
+                         int32_t planes, const float* lr, float beta1, float beta2, float eps, int32_t step,
+                         void* stream);
+
 /* ---- NEXT-1: latent-space ensemble disagreement (PAPER.md eq:w2_pixel,
    §3.3) ---------------------------------------------------------------
    For each candidate view v: W2 = (1/(H_z W_z)) sum_p (1/C(M,2)) sum_{i<j}
@@ -315,7 +333,8 @@ enum {
   GSR_STAGE_W2 = 10,        /* NEXT-1 latent W2 scorer */
   GSR_STAGE_SOBEL = 11,     /* NEXT-4 Sobel image term */
   GSR_STAGE_BACKWARD = 12,  /* NEXT-3 backward rasterizer (K6b + K1b) */
-  GSR_N_STAGES = 13
+  GSR_STAGE_OPTIM = 13,     /* NEXT-3 loss gradient + Adam step */
+  GSR_N_STAGES = 14
 };
 /* enable != 0: bracket every stage with CUDA events on its launch stream. */
 gsr_status gsr_timing_enable(gsr_ctx* ctx, int enable);

@@ -8,6 +8,8 @@
 #include <cuda_fp16.h>
 #include <stdint.h>
 
+#include <algorithm>
+#include <cmath>
 #include <string>
 #include <vector>
 
@@ -98,6 +100,7 @@ enum Slot {
   S_GRAD2D,                                 // NEXT-3 per-(view, g) 2D gradients
   S_CSH, S_CSMETA,                          // K4c chunk x tile offsets, view / chunk table
   S_K6ORDER,                                // K6 launch order (largest tiles first)
+  S_OPTIM,                                  // NEXT-3 loss partial sums
   S_NSLOTS
 };
 

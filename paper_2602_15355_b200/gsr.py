@@ -33,9 +33,9 @@ EXPORTED = ["gsr_create", "gsr_destroy", "gsr_last_error", "gsr_version", "gsr_c
             "gsr_project", "gsr_bin_sort", "gsr_composite", "gsr_score_views", "gsr_select_nbv",
             "gsr_sort_pairs_u64", "gsr_scratch_bytes", "gsr_timing_enable", "gsr_timing_read", "gsr_w2_scores",
             "gsr_sobel_scores", "gsr_backward", "gsr_order_cache_size", "gsr_build_order_cache",
-            "gsr_bin_sort_cached"]
+            "gsr_bin_sort_cached", "gsr_l2_loss", "gsr_adam_step"]
 STAGES = ["project", "compact", "depth_sort", "emit", "ranges", "tile_sort", "composite", "score", "select",
-          "sort_u64", "w2", "sobel", "backward"]
+          "sort_u64", "w2", "sobel", "backward", "optim"]
 
 
 class GsrError(RuntimeError):
@@ -72,6 +72,8 @@ def _load():
     L.gsr_composite.argtypes = [P, P, i64, P, P, P, i32, P, P, P, P, P, P, P]
     L.gsr_sobel_scores.argtypes = [P, P, P, i32, P, P, P]
     L.gsr_backward.argtypes = [P, P, P, i32, P, P, P, P, P, P, P, P, P]
+    L.gsr_l2_loss.argtypes = [P, P, P, i64, P, P, P, P]
+    L.gsr_adam_step.argtypes = [P, P, P, P, P, i64, i32, P, ctypes.c_float, ctypes.c_float, ctypes.c_float, i32, P]
     L.gsr_order_cache_size.argtypes = [P, i32, P]
     L.gsr_order_cache_size.restype = i64
     L.gsr_build_order_cache.argtypes = [P, P, P, i32, P, P, P]
@@ -283,6 +285,26 @@ def gsr_backward(ctx: Context, g: Gaussians, cams, render_rec, bin_rec, vals, ra
     ctx._check(lib.gsr_backward(ctx.handle, ctypes.byref(gs), c.ctypes.data, len(c),
                                 ctypes.byref(ls) if ls is not None else None, _ptr(render_rec), _ptr(bin_rec),
                                 _ptr(vals), _ptr(ranges), _ptr(rgbu), _ptr(dl_drgbu), _ptr(grads), _stream(stream)))
+
+
+def gsr_l2_loss(ctx: Context, img, target, weights, dl_dimg=None, loss=None, stream=None):
+    """NEXT-3: L2 photometric loss over (r, g, b, U) pixels (+ its gradient)."""
+    import torch
+    w = np.ascontiguousarray(np.asarray(weights, dtype=np.float32).reshape(4))
+    if loss is None:
+        loss = torch.zeros(1, dtype=torch.float64, device=img.device)
+    ctx._check(lib.gsr_l2_loss(ctx.handle, _ptr(img), _ptr(target), int(img.numel() // 4), w.ctypes.data,
+                               _ptr(dl_dimg), _ptr(loss), _stream(stream)))
+    return loss
+
+
+def gsr_adam_step(ctx: Context, params, grads, m, v, lr, step: int, beta1=0.9, beta2=0.999, eps=1e-8,
+                  stream=None):
+    """NEXT-3: projected Adam on the field planes [P][n][4] (lr [P][4] host)."""
+    P, n = int(params.shape[0]), int(params.shape[1])
+    lr = np.ascontiguousarray(np.asarray(lr, dtype=np.float32).reshape(P, 4))
+    ctx._check(lib.gsr_adam_step(ctx.handle, _ptr(params), _ptr(grads), _ptr(m), _ptr(v), n, P, lr.ctypes.data,
+                                 beta1, beta2, eps, step, _stream(stream)))
 
 
 def gsr_sobel_scores(ctx: Context, gray, cams, tile_partial, scores, stream=None):

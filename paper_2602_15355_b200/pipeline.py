@@ -294,3 +294,39 @@ class Renderer:
         gsr.gsr_backward(self.ctx, self.field, self._cams, self.rec, self.bin, self.vals, self.ranges, self.rgbu,
                          dl_drgbu.contiguous(), grads, lod=self.lod, stream=stream)
         return grads
+
+
+class Refiner:
+    """NEXT-3 UPDATE_GS refinement (Alg. 1, "bounded refinement
+    (5k iterations per inserted image)", §4.1): per step, render the
+    captured poses (Renderer.forward), the L2 photometric loss gradient
+    against the captures, the backward rasterizer, and one projected Adam
+    step on the field's planes -- all in libgsr kernels.  ``lr`` is a
+    learning rate per (plane, component); the field is updated in place."""
+
+    def __init__(self, field: Gaussians, lr, weights=(1.0, 1.0, 1.0, 0.0), lod: Optional[gsr.Lod] = None,
+                 betas=(0.9, 0.999), eps: float = 1e-8):
+        self.field = field
+        self.renderer = Renderer(field, lod)
+        self.lr = np.asarray(lr, dtype=np.float32).reshape(field.planes.shape[0], 4)
+        self.weights = np.asarray(weights, dtype=np.float32)
+        self.m = torch.zeros_like(field.planes)
+        self.v = torch.zeros_like(field.planes)
+        self.grads = torch.zeros_like(field.planes)
+        self.betas, self.eps, self.t = betas, eps, 0
+        self.loss = torch.zeros(1, dtype=torch.float64, device=field.planes.device)
+
+    def step(self, cams, targets: torch.Tensor) -> torch.Tensor:
+        """One refinement iteration on the poses ``cams`` (<= 64, one
+        resolution) with capture images ``targets`` [V][H][W][4]; returns the
+        pre-update loss (device scalar)."""
+        img = self.renderer.forward(cams)
+        dl = torch.empty_like(img)
+        ctx = self.renderer.ctx
+        gsr.gsr_l2_loss(ctx, img, targets.contiguous(), self.weights, dl_dimg=dl, loss=self.loss)
+        self.grads.zero_()
+        self.renderer.backward(dl, self.grads)
+        self.t += 1
+        gsr.gsr_adam_step(ctx, self.field.planes, self.grads, self.m, self.v, self.lr, self.t,
+                          self.betas[0], self.betas[1], self.eps)
+        return self.loss
