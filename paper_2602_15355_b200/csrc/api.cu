@@ -84,6 +84,7 @@ gsr_status gsr_create(gsr_ctx** out, int device) {
   if (const char* v = std::getenv("GSR_PIX")) c->composite_pix = std::atoi(v);
   if (const char* v = std::getenv("GSR_KPT")) c->sort_kpt32 = std::atoi(v);
   if (const char* v = std::getenv("GSR_DKEY64")) c->depth_keys64 = std::atoi(v) != 0;
+  if (const char* v = std::getenv("GSR_BWRED")) c->bw_reduce = std::atoi(v);
   if (const char* v = std::getenv("GSR_K6ORDER")) c->k6_order = std::atoi(v) != 0;
   if (const char* v = std::getenv("GSR_TSORT")) c->tile_sort_radix = std::string(v) == "radix";
   e = cudaMallocHost(&c->host_pinned, 4096);

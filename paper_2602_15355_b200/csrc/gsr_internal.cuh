@@ -129,6 +129,7 @@ struct gsr_ctx {
   int composite_stages = 4;   // K6 ring depth (GSR_STAGES: 4 or 8)
   int composite_pix = 1;      // K6 pixels per consumer lane (GSR_PIX: 1 or 2)
   bool depth_keys64 = false;  // force the 64-bit depth-sort keys (GSR_DKEY64=1)
+  int bw_reduce = 2;          // K6b warp reduction: 0 shuffle trees, 1 smem atomics, 2 butterfly (GSR_BWRED)
   bool k6_order = false;      // K6 largest-tile-first launch order (GSR_K6ORDER=1)
   bool tile_sort_radix = false;  // K4b two onesweep passes instead of the K4c counting scatter (GSR_TSORT=radix)
   int composite_variant = 6;  // K6: 1 block-sync LDG, 2 TMA bulk/record, 3 TMA gather4, 4 cp.async, 5 warp-independent LDG, 6 = 5 + exact ellipse-box cull (default), 7 = 6 with per-warp TMA gather4 buffers (GSR_STAGES: 2 or 4)

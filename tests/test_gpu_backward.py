@@ -78,3 +78,16 @@ def test_renderer_api_matches_oracle(ctx):
     G = np.random.default_rng(8).normal(size=ref_img.shape).astype(np.float32)
     got = r.backward(torch.from_numpy(G).cuda()).cpu().numpy()
     _compare(got, bw.backward_views(fld, cams, G), 3)
+
+
+@pytest.mark.parametrize("red", ["0", "2"])
+def test_backward_reduction_variants(ctx, red, monkeypatch):
+    """K6b's warp reductions (shuffle trees / transposed butterfly, GSR_BWRED)
+    give the same gradients within the float tolerance."""
+    from paper_2602_15355_b200 import Context
+    monkeypatch.setenv("GSR_BWRED", red)
+    c = Context(0)
+    fld, cams = synth.random_scene_small(8, 150, 40, 33, 40.0, 2, 2, logscale_mu=-2.4)
+    G = np.random.default_rng(9).normal(size=(2, 33, 40, 4)).astype(np.float32)
+    img, got = gpu_forward_backward(c, fld, cams, G)
+    _compare(got, bw.backward_views(fld, cams, G), 2)
