@@ -527,7 +527,7 @@ def main():
             "stages": stage_tab,
             "gpu_launches": int(launches * world), "clocks": clk, "e2e": e2e,
             "keys_per_step_rank0": int(sum(scorer.last_keys))}
-    if rank == 0 and not args.no_extras:
+    if rank == 0 and world == 1 and not args.no_extras:  # single-GPU extras (skipped in the scaling runs)
         line["next1_w2"] = bench_w2(gsr, dev, peaks)
         line["next4_sobel"] = bench_sobel(gsr, dev, peaks)
         line["next3_backward"] = bench_backward(G, dev)
