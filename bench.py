@@ -374,10 +374,19 @@ def main():
     from paper_2602_15355_b200.distributed import broadcast_field, score_and_select
     from paper_2602_15355_b200.pipeline import ViewScorer
 
+    # GSR_BENCH_BACKEND=gloo: functional check of the N > 1 code path on a box
+    # with fewer GPUs than ranks (ranks share devices; host-mediated
+    # collectives; its timings are not scaling numbers)
+    backend = os.environ.get("GSR_BENCH_BACKEND", "nccl")
+    if backend != "nccl":
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     scene = synth.make_scene(CONFIG_ID) if rank == 0 else synth.make_scene(CONFIG_ID, n_override=1, views=1024)
     P = 3 + synth.n_sh_planes(3)
     n = 1_000_000
