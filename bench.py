@@ -348,6 +348,41 @@ def bench_hierarchical(dev, reps: int = 2):
             "nbv": int(nbv), "config": "c5: 2M Gaussians, 4096 coarse views 256^2 -> top-64 fine 1024^2"}
 
 
+def bench_configs(dev, steps: int = 3):
+    """Views/s of every BASELINE.json config on one GPU (the headline line is
+    configs[2]; configs[3] and [4] also appear in next2_wang /
+    c5_hierarchical): c1 10k / 16 views 128^2, c2 200k terrain / 256 views
+    512^2, c4 8M Wang assembly / 64 fly-over views 1920x1080."""
+    import torch
+    import synth
+    from paper_2602_15355_b200 import Gaussians
+    from paper_2602_15355_b200.pipeline import ViewScorer
+    out = {}
+    for cfg in (1, 2, 4):
+        sc = synth.make_scene(cfg)
+        G = Gaussians(torch.from_numpy(sc.field.planes).to(dev), sc.field.sh_degree)
+        s = ViewScorer(G, batch_views=16, n_slots=2)
+        nv = len(sc.cameras)
+        for _ in range(2):
+            s.score_views(sc.cameras)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.reset_counters()
+        e0.record()
+        for _ in range(steps):
+            s.score_views(sc.cameras)
+        e1.record()
+        torch.cuda.synchronize()
+        t = e0.elapsed_time(e1) / steps / 1e3
+        fr = float(s.n_frag[0].item()) / steps
+        out[synth.CONFIG_NAMES[cfg]] = {"views_per_sec": round(nv / t, 1), "ms_per_pass": round(t * 1e3, 2),
+                                        "fragments_per_sec": round(fr / t, 1),
+                                        "keys_per_view": int(sum(s.last_keys) / nv)}
+        del s, G, sc
+        torch.cuda.empty_cache()
+    return out
+
+
 # ----------------------------------------------------------------------------- GPU arm
 def main():
     args = parse()
@@ -542,6 +577,7 @@ def main():
         line["next3_backward"] = bench_backward(G, dev)
         line["next2_wang"] = bench_wang(dev)
         line["c5_hierarchical"] = bench_hierarchical(dev)
+        line["configs"] = bench_configs(dev)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(scene, args.cpu_views)
     if rank == 0:

@@ -1002,6 +1002,7 @@ __global__ void __launch_bounds__(1024) k5_ranges(const uint32_t* __restrict__ c
 constexpr int CS_KPT = 8;
 constexpr int CS_CHUNK = 32768;
 constexpr int CS_MAX_TPV = 12288;
+constexpr int CS_AUTO_TPV = 4352;
 
 // view / chunk bookkeeping (K5 tail): vs[v] = first key of view v (vs[V] = K),
 // pb[v] = first chunk of view v (pb[V] = chunks)
@@ -1652,7 +1653,13 @@ static gsr_status bin_sort_impl(gsr_ctx* ctx, const uint32_t* bin_rec, int64_t n
   if ((s = check_cuda(ctx, cudaGetLastError(), "k5_ranges")) != GSR_OK) return s;
 
   // ---- K4b / K4c: tile sort ----
-  if (tpv <= (uint64_t)CS_MAX_TPV && !ctx->tile_sort_radix) {
+  // K4c when 8 warps' counters fit next to 2 resident blocks per SM (measured:
+  // 2,500 tiles/view c3 and 4,096 c5-fine faster than the radix passes; 8,160
+  // c4 slower with 4 warps and 1 block per SM); GSR_TSORT=cs / radix forces
+  const bool use_cs = ctx->tile_sort_mode == 1 ? tpv <= (uint64_t)CS_MAX_TPV
+                      : ctx->tile_sort_mode == 2 ? false
+                                                 : tpv <= (uint64_t)CS_AUTO_TPV;
+  if (use_cs) {
     // K4c counting scatter (default)
     const uint64_t nchunks_max = (uint64_t)(K + CS_CHUNK - 1) / CS_CHUNK + (uint64_t)n_views;
     void *hm, *meta;
