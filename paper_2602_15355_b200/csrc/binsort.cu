@@ -1085,7 +1085,8 @@ template <int W>
 __global__ void __launch_bounds__(W * 32) cs_scatter(const uint32_t* __restrict__ tkeys,
                                                      const uint32_t* __restrict__ tvals,
                                                      const uint32_t* __restrict__ meta, int V, uint32_t tpv,
-                                                     int dbits, const uint32_t* __restrict__ H,
+                                                     int dbits, uint32_t tslice, int nslice,
+                                                     const uint32_t* __restrict__ H,
                                                      uint32_t* __restrict__ vals_out, uint64_t* __restrict__ keys64,
                                                      const uint32_t* __restrict__ depth_plane, int64_t nper) {
   // shared memory: s_base [tpv] u32 (chunk offset + keys so far), s_sub [tpv]
@@ -1094,19 +1095,23 @@ __global__ void __launch_bounds__(W * 32) cs_scatter(const uint32_t* __restrict_
   // per-warp rows are padded to a multiple of 8 tiles (16 B) so the prefix
   // loop can work on packed u16 pairs and the reset on 16-byte stores
   extern __shared__ uint32_t smem[];
-  const uint32_t ts = (tpv + 7u) & ~7u;  // row stride (u16 elements)
+  // blocks (chunk, slice): the slice's tiles [tb, tb + tn) only (large tile
+  // counts are split so 8 warps' counters fit in shared memory)
+  const uint32_t chunk = blockIdx.x / nslice;
+  const uint32_t tb = (blockIdx.x - chunk * nslice) * tslice;
+  const uint32_t tn = min(tslice, tpv - tb);
+  const uint32_t ts = (tn + 7u) & ~7u;  // row stride (u16 elements)
   uint32_t* s_base = smem;
   uint32_t* s_sub = smem + ts;
   uint16_t* s_wh = reinterpret_cast<uint16_t*>(smem + 2 * ts);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const uint32_t chunk = blockIdx.x;
   if (chunk >= meta[(V + 1) + V]) return;
   int v;
   uint32_t k0, k1;
   cs_locate(meta, V, chunk, v, k0, k1);
-  const uint32_t vb = (uint32_t)v * tpv;
-  const uint32_t* Hrow = H + (size_t)chunk * tpv;
-  for (uint32_t d = tid; d < tpv; d += W * 32) s_base[d] = Hrow[d];
+  const uint32_t vb = (uint32_t)v * tpv + tb;
+  const uint32_t* Hrow = H + (size_t)chunk * tpv + tb;
+  for (uint32_t d = tid; d < tn; d += W * 32) s_base[d] = Hrow[d];
   for (uint32_t i = tid; i < (uint32_t)W * ts / 8; i += W * 32) reinterpret_cast<uint4*>(s_wh)[i] = make_uint4(0, 0, 0, 0);
   __syncthreads();
   const uint32_t lt = (1u << lane) - 1u;
@@ -1118,15 +1123,13 @@ __global__ void __launch_bounds__(W * 32) cs_scatter(const uint32_t* __restrict_
 #pragma unroll
     for (int k = 0; k < CS_KPT; ++k) {
       const uint32_t i = wb + k * 32 + lane;
-      const bool ok = i < k1;
-      dg[k] = ok ? __ldg(tkeys + i) - vb : 0u;
-      vv[k] = ok ? __ldg(tvals + i) : 0u;
+      dg[k] = i < k1 ? __ldg(tkeys + i) - vb : 0xffffffffu;  // out of the slice: >= tn
+      vv[k] = (i < k1 && dg[k] < tn) ? __ldg(tvals + i) : 0u;
     }
     // warp-local stable ranks: lanes holding the same tile digit (ballots per bit)
 #pragma unroll
     for (int k = 0; k < CS_KPT; ++k) {
-      const uint32_t i = wb + k * 32 + lane;
-      const bool ok = i < k1;
+      const bool ok = dg[k] < tn;
       uint32_t peers = __ballot_sync(FULL, ok);
       for (int b = 0; b < dbits; ++b) {
         const bool bit = (dg[k] >> b) & 1u;
@@ -1154,12 +1157,12 @@ __global__ void __launch_bounds__(W * 32) cs_scatter(const uint32_t* __restrict_
         run += c;
       }
       const uint32_t d = 2 * p;
-      if (d < tpv) {
+      if (d < tn) {
         const uint32_t b = s_base[d];
         s_sub[d] = b;
         s_base[d] = b + (run & 0xffffu);
       }
-      if (d + 1 < tpv) {
+      if (d + 1 < tn) {
         const uint32_t b = s_base[d + 1];
         s_sub[d + 1] = b;
         s_base[d + 1] = b + (run >> 16);
@@ -1168,8 +1171,7 @@ __global__ void __launch_bounds__(W * 32) cs_scatter(const uint32_t* __restrict_
     __syncthreads();
 #pragma unroll
     for (int k = 0; k < CS_KPT; ++k) {
-      const uint32_t i = wb + k * 32 + lane;
-      if (i < k1) {
+      if (dg[k] < tn) {
         const uint32_t pos = s_sub[dg[k]] + (uint32_t)wh[dg[k]] + rk[k];
         vals_out[pos] = vv[k];
         if (keys64) keys64[pos] = ((uint64_t)(vb + dg[k]) << 32) | __ldg(depth_plane + (int64_t)v * nper + vv[k]);
@@ -1653,38 +1655,33 @@ static gsr_status bin_sort_impl(gsr_ctx* ctx, const uint32_t* bin_rec, int64_t n
   if ((s = check_cuda(ctx, cudaGetLastError(), "k5_ranges")) != GSR_OK) return s;
 
   // ---- K4b / K4c: tile sort ----
-  // K4c when 8 warps' counters fit next to 2 resident blocks per SM (measured:
-  // 2,500 tiles/view c3 and 4,096 c5-fine faster than the radix passes; 8,160
-  // c4 slower with 4 warps and 1 block per SM); GSR_TSORT=cs / radix forces
-  const bool use_cs = ctx->tile_sort_mode == 1 ? tpv <= (uint64_t)CS_MAX_TPV
-                      : ctx->tile_sort_mode == 2 ? false
-                                                 : tpv <= (uint64_t)CS_AUTO_TPV;
+  // K4c (default, up to CS_MAX_TPV tiles per view: cs_hist keeps one view's
+  // counters in 48 KB of shared memory); tile counts above CS_AUTO_TPV are
+  // split into slices so 8 warps' scatter counters still fit twice per SM
+  // (measured: c3 2,500 tiles 1.09 -> 0.79 ms per batch; c4 8,160 tiles in 2
+  // slices 804 vs 799 views/s for the radix passes; unsliced with 4 warps 609).
+  // GSR_TSORT=radix forces the two onesweep passes.
+  const bool use_cs = ctx->tile_sort_mode != 2 && tpv <= (uint64_t)CS_MAX_TPV;
   if (use_cs) {
     // K4c counting scatter (default)
     const uint64_t nchunks_max = (uint64_t)(K + CS_CHUNK - 1) / CS_CHUNK + (uint64_t)n_views;
     void *hm, *meta;
     if ((s = ensure(ctx, S_CSH, nchunks_max * tpv * 4, &hm)) != GSR_OK) return s;
     if ((s = ensure(ctx, S_CSMETA, 2 * (n_views + 1) * 4, &meta)) != GSR_OK) return s;
-    const int W = (24 * tpv <= 100 * 1024) ? 8 : 4;
-    const size_t smem = (size_t)((tpv + 7) & ~7ull) * (8 + 2 * W);
+    const int nslice = (int)((tpv + CS_AUTO_TPV - 1) / CS_AUTO_TPV);
+    const uint32_t tslice = (uint32_t)((tpv + nslice - 1) / nslice);
+    const size_t smem = (size_t)((tslice + 7) & ~7u) * (8 + 2 * 8);
     sp = stage_begin(ctx, GSR_STAGE_TILE_SORT, st);
     cs_meta<<<1, 32, 0, st>>>((const uint2*)ranges, n_views, (uint32_t)tpv, (uint32_t)K, (uint32_t*)meta);
     cs_hist<<<(unsigned)nchunks_max, 256, tpv * 4, st>>>((const uint32_t*)tka, (const uint32_t*)meta, n_views,
                                                           (uint32_t)tpv, (uint32_t*)hm);
     cs_scan<<<(unsigned)((T + 255) / 256), 256, 0, st>>>((const uint2*)ranges, (const uint32_t*)meta, n_views,
                                                          (uint32_t)tpv, (uint32_t*)hm);
-    const int dbits = std::max(1, bits_for(tpv));
-    if (W == 8) {
-      cudaFuncSetAttribute(cs_scatter<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      cs_scatter<8><<<(unsigned)nchunks_max, 256, smem, st>>>((const uint32_t*)tka, (const uint32_t*)tva,
-                                                              (const uint32_t*)meta, n_views, (uint32_t)tpv, dbits,
-                                                              (const uint32_t*)hm, vals, keys, p_depth, n);
-    } else {
-      cudaFuncSetAttribute(cs_scatter<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      cs_scatter<4><<<(unsigned)nchunks_max, 128, smem, st>>>((const uint32_t*)tka, (const uint32_t*)tva,
-                                                              (const uint32_t*)meta, n_views, (uint32_t)tpv, dbits,
-                                                              (const uint32_t*)hm, vals, keys, p_depth, n);
-    }
+    const int dbits = std::max(1, bits_for(tslice));
+    cudaFuncSetAttribute(cs_scatter<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cs_scatter<8><<<(unsigned)(nchunks_max * nslice), 256, smem, st>>>(
+        (const uint32_t*)tka, (const uint32_t*)tva, (const uint32_t*)meta, n_views, (uint32_t)tpv, dbits, tslice,
+        nslice, (const uint32_t*)hm, vals, keys, p_depth, n);
     stage_end(ctx, sp, st);
     // hist reads 4 B/key; scatter reads 8 B/key and writes the 4-B values
     // (+ 8-B keys when asked); the chunk x tile matrix is written, scanned in
