@@ -327,7 +327,7 @@ def bench_hierarchical(dev, reps: int = 2):
     from paper_2602_15355_b200.pipeline import ViewScorer
     sc = synth.make_scene(5)
     G = Gaussians(torch.from_numpy(sc.field.planes).to(dev), sc.field.sh_degree)
-    coarse = ViewScorer(G, batch_views=64, n_slots=2)
+    coarse = ViewScorer(G, batch_views=32, n_slots=2)  # measured: 32 > 64 > 16 views per batch at 256^2
     fine = ViewScorer(G, batch_views=16, n_slots=2)
 
     def run():
