@@ -50,7 +50,7 @@ def test_adam_steps_vs_oracle(ctx):
 def test_refinement_recovers_a_perturbed_field(ctx):
     """Captures = renders of the true field from 4 poses; the field with
     perturbed colours, opacities and positions is refined for 60 steps: the
-    photometric loss drops by > 80 %."""
+    photometric loss drops by > 98 % (measured 0.0125 -> 6.4e-5)."""
     from paper_2602_15355_b200.pipeline import Refiner, Renderer
     fld, cams = synth.random_scene_small(3, 300, 64, 48, 55.0, 4, 0, logscale_mu=-2.4)
     true = to_dev(fld)
@@ -66,4 +66,5 @@ def test_refinement_recovers_a_perturbed_field(ctx):
     lr[3] = [2e-2, 2e-2, 2e-2, 2e-2]   # DC colour
     ref = Refiner(G, lr)
     losses = [ref.step(cams, targets).item() for _ in range(60)]
-    assert losses[-1] < 0.2 * losses[0], (losses[0], losses[-1])
+    print("refinement loss", losses[0], "->", losses[-1])
+    assert losses[-1] < 0.02 * losses[0], (losses[0], losses[-1])  # measured ~0.005
