@@ -252,6 +252,23 @@ def test_measured_variants_stay_exact(env, monkeypatch):
     assert np.array_equal(g["rgbu"], o["rgbu"])
 
 
+@pytest.mark.parametrize("W,H,env", [(1200, 1000, ""), (1200, 1000, "GSR_TSORT=radix"), (1800, 1760, "")])
+def test_large_tile_counts(W, H, env, monkeypatch):
+    """Tile counts past the K4c slice size (4,352 tiles: 75 x 63 = 4,725 tiles
+    in 2 slices; and the same through the radix passes) and past the
+    counting-scatter limit (12,288: 113 x 110 = 12,430 tiles take the radix
+    tile sort): bit-exact keys, order, ranges and images."""
+    from paper_2602_15355_b200 import Context
+    for kv in env.split():
+        k, v = kv.split("=")
+        monkeypatch.setenv(k, v)
+    c = Context(0)
+    fld, cams = synth.random_scene_small(12, 6000, W, H, 0.9 * W, 2, 1, logscale_mu=-4.0)
+    g, o = _full_check(c, fld, cams)
+    assert g["K"] > 20000
+    assert np.array_equal(g["rgbu"], o["rgbu"])
+
+
 def test_empty_field_and_huge_gaussian(ctx):
     """n = 0 (empty field) scores 0 through ViewScorer; one Gaussian larger
     than the image (every tile, many rows / long spans in K1 and K3) plus small
