@@ -25,11 +25,19 @@ constexpr float SH_C3c = 0.4570457995f;
 constexpr float SH_C3d = 0.3731763326f;
 constexpr float SH_C3e = 1.4453057213f;
 
+// SH coefficients of the thread's Gaussian, parked in shared memory (plane j
+// of thread t at s[j * 256 + t]: conflict-free float4 accesses) instead of
+// 48 registers across the view loop; each thread reads only its own
+// coefficients, so no barrier is needed.
 template <int DEG>
 struct ShCoef {
   static constexpr int kCoef = (DEG + 1) * (DEG + 1);
   static constexpr int kPlanes = (3 * kCoef + 3) / 4;
-  float k[kPlanes * 4];
+  const float4* s;  // this thread's plane 0
+  __device__ __forceinline__ float k(int i) const {
+    const float4 c = s[(i >> 2) * 256];
+    return (i & 3) == 0 ? c.x : (i & 3) == 1 ? c.y : (i & 3) == 2 ? c.z : c.w;
+  }
 };
 
 // rgb_ch = max(0, ((k0 + Y1 k1) + Y2 k2) + ...), Y0 = 1 (DC is the colour).
@@ -62,9 +70,9 @@ __device__ __forceinline__ void sh_colour(const ShCoef<DEG>& S, float x, float y
   }
 #pragma unroll
   for (int ch = 0; ch < 3; ++ch) {
-    float acc = S.k[ch];
+    float acc = S.k(ch);
 #pragma unroll
-    for (int c = 1; c < ShCoef<DEG>::kCoef; ++c) acc = acc + Y[c] * S.k[3 * c + ch];
+    for (int c = 1; c < ShCoef<DEG>::kCoef; ++c) acc = acc + Y[c] * S.k(3 * c + ch);
     rgb[ch] = fmaxf(0.0f, acc);
   }
 }
@@ -76,17 +84,16 @@ __global__ void __launch_bounds__(256) k1_project(const float4* __restrict__ po,
                                                   const __grid_constant__ CamBatch cams,
                                                   const __grid_constant__ LodParams lod,
                                                   float4* __restrict__ rec, uint32_t* __restrict__ bin) {
+  __shared__ float4 s_sh[ShCoef<DEG>::kPlanes * 256];
   const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (g >= n) return;
   const float4 P = __ldg(po + g);
   const float4 Sd = __ldg(su + g);
   const float4 Q4 = __ldg(rq + g);
   ShCoef<DEG> S;
+  S.s = s_sh + threadIdx.x;
 #pragma unroll
-  for (int j = 0; j < ShCoef<DEG>::kPlanes; ++j) {
-    const float4 c = __ldg(sh + (int64_t)j * n + g);
-    S.k[4 * j + 0] = c.x; S.k[4 * j + 1] = c.y; S.k[4 * j + 2] = c.z; S.k[4 * j + 3] = c.w;
-  }
+  for (int j = 0; j < ShCoef<DEG>::kPlanes; ++j) s_sh[j * 256 + threadIdx.x] = __ldg(sh + (int64_t)j * n + g);
   const float mx = P.x, my = P.y, mz = P.z, o0 = P.w;
   float4 TL = make_float4(0.f, 0.f, 0.f, 0.f);
   int level = 0;
