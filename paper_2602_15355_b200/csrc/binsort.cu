@@ -147,8 +147,12 @@ __global__ void __launch_bounds__(256) k2_compact(const uint32_t* __restrict__ d
                                                   int dpasses, int dshift, uint32_t dbase) {
   __shared__ uint32_t s_hist[5][256];
   __shared__ uint64_t s_wv[8], s_wk[8];
-  __shared__ uint64_t s_pv, s_pk;
+  __shared__ uint64_t s_pv, s_pk, s_tv;
   __shared__ uint32_t s_bid;
+  // the block's visible (key, g) pairs, compacted here first so the global
+  // writes are coalesced
+  __shared__ KeyT s_key[K2_TILE];
+  __shared__ uint32_t s_g[K2_TILE];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (tid == 0) s_bid = atomicAdd(ctr, 1u);
   for (int i = tid; i < 5 * 256; i += 256) (&s_hist[0][0])[i] = 0;
@@ -183,36 +187,49 @@ __global__ void __launch_bounds__(256) k2_compact(const uint32_t* __restrict__ d
       if (lane == 0) { publish(lb_vis, bid, LB_INC | (pv + tv)); publish(lb_k, bid, LB_INC | (pk + tk)); }
     }
     if (lane == 0) {
-      s_pv = pv; s_pk = pk;
+      s_pv = pv; s_pk = pk; s_tv = tv;
       if ((bid + 1) * K2_TILE >= M) { totals[0] = pv + tv; totals[1] = pk + tk; }
     }
   }
   __syncthreads();
-  uint64_t pv = s_pv + s_wv[warp] + (iv - cv);
+  uint32_t lv = (uint32_t)(s_wv[warp] + (iv - cv));  // block-local slot
   uint64_t pk = s_pk + s_wk[warp] + (ik - ck);
+  // (view, g) of i0 with one division per thread, then stepped
+  uint64_t view = i0 < M ? (uint64_t)(i0 / n) : 0;
+  int64_t g = i0 - (int64_t)view * n;
+  bool wide_miss = false;
 #pragma unroll
   for (int k = 0; k < K2_ITEMS; ++k) {
     const int64_t i = i0 + k;
     if (i >= M) break;
+    if (g == n) { g = 0; ++view; }
     if (emit_off) emit_off[i] = (uint32_t)pk;
     if (nt[k]) {
-      const uint64_t view = (uint64_t)(i / n);
-      const uint32_t g = (uint32_t)(i - (int64_t)view * n);
       const uint32_t d = __ldg(depth_plane + i);
       KeyT key;
       if (sizeof(KeyT) == 8) {
         key = (KeyT)((view << 32) | d);
       } else {
         const uint32_t off = d - dbase;
-        if (off >> dshift) totals[2] = 1;  // does not fit: caller falls back to 64-bit keys
+        wide_miss |= (off >> dshift) != 0;  // does not fit: caller falls back to 64-bit keys
         key = (KeyT)(((uint32_t)view << dshift) | off);
       }
-      dkeys[pv] = key;
-      dvals[pv] = g;
-      for (int p = 0; p < dpasses; ++p) atomicAdd(&s_hist[p][(uint32_t)(key >> (8 * p)) & 255], 1u);
-      ++pv;
+      s_key[lv] = key;
+      s_g[lv] = (uint32_t)g;
+      ++lv;
     }
     pk += nt[k];
+    ++g;
+  }
+  if (wide_miss) totals[2] = 1;
+  __syncthreads();
+  const uint32_t bt = (uint32_t)s_tv;
+  const uint64_t pv0 = s_pv;
+  for (uint32_t j = tid; j < bt; j += 256) {
+    const KeyT key = s_key[j];
+    dkeys[pv0 + j] = key;
+    dvals[pv0 + j] = s_g[j];
+    for (int p = 0; p < dpasses; ++p) atomicAdd(&s_hist[p][(uint32_t)(key >> (8 * p)) & 255], 1u);
   }
   __syncthreads();
   for (int i = tid; i < dpasses * 256; i += 256) {
