@@ -127,7 +127,7 @@ __device__ __forceinline__ void publish(uint64_t* words, int64_t bid, uint64_t v
 // ---------------------------------------------------------------------------
 // K2: compact visible (view, g) pairs, K and visible-count totals.
 // Block tile = 256 threads x 8 consecutive items.
-constexpr int K2_ITEMS = 8;
+constexpr int K2_ITEMS = 12;
 constexpr int K2_TILE = 256 * K2_ITEMS;
 
 // KeyT = uint64_t: key = view << 32 | depth bits.  KeyT = uint32_t (the
