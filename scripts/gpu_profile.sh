@@ -10,7 +10,7 @@ $CMD > gpurun_out/plain_$TAG.log 2>&1 || { echo "plain run failed"; tail -20 gpu
 ncu --metrics gpu__time_duration.sum --clock-control none -s 300 -c 400 --csv \
     --log-file gpurun_out/launches_$TAG.csv $CMD > gpurun_out/ncu_launch_$TAG.log 2>&1
 echo "launch list rc=$?"
-ncu --set full --clock-control none --import-source on -k regex:"$KRE" -s 40 -c 8 \
+ncu --set full --clock-control none --import-source on -k regex:"$KRE" -s 40 -c ${NCOUNT:-8} \
     -o gpurun_out/prof_$TAG $CMD > gpurun_out/ncu_full_$TAG.log 2>&1
 echo "full capture rc=$?"
 ls -la gpurun_out/
