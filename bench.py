@@ -561,6 +561,32 @@ def main():
         del iso_scorer
         torch.cuda.empty_cache()
 
+    # the two collectives timed on their own (CUDA events on
+    # the current stream, max over ranks): C1 broadcast of the 240 MB field
+    # and C2 all-gather of the scores (both are inside every timed step above)
+    coll = None
+    if world > 1:
+        from paper_2602_15355_b200.distributed import gather_scores
+        reps = 5
+        loc = torch.zeros((1024 + world - 1) // world, dtype=torch.float32, device=dev)
+        barrier()
+        e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+        e0.record()
+        for _ in range(reps):
+            broadcast_field(planes)
+        e1.record()
+        for _ in range(reps):
+            gather_scores(loc, 1024)
+        e2.record()
+        barrier()
+        ct = torch.tensor([e0.elapsed_time(e1) / reps, e1.elapsed_time(e2) / reps], dtype=torch.float64,
+                          device=dev)
+        dist.all_reduce(ct, op=dist.ReduceOp.MAX)
+        bms, gms = float(ct[0].item()), float(ct[1].item())
+        coll = {"backend": backend, "broadcast_ms": round(bms, 4),
+                "broadcast_GB_per_s": round(planes.numel() * 4 / (bms / 1e3) / 1e9, 1),
+                "all_gather_ms": round(gms, 4), "bytes_broadcast": int(planes.numel() * 4)}
+
     line = {"metric": METRIC, "value": round(views_per_s, 2), "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 3),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
@@ -569,7 +595,7 @@ def main():
             "wall_ms_per_step": round(wall_ms / args.steps, 3), "roofline": roof, "roofline_isolated": iso,
             "roofline_sort": roof_sort,
             "stages": stage_tab,
-            "gpu_launches": int(launches * world), "clocks": clk, "e2e": e2e,
+            "gpu_launches": int(launches * world), "clocks": clk, "e2e": e2e, "collectives": coll,
             "keys_per_step_rank0": int(sum(scorer.last_keys))}
     if rank == 0 and world == 1 and not args.no_extras:  # single-GPU extras (skipped in the scaling runs)
         line["next1_w2"] = bench_w2(gsr, dev, peaks)
