@@ -86,6 +86,7 @@ gsr_status gsr_create(gsr_ctx** out, int device) {
   if (const char* v = std::getenv("GSR_DKEY64")) c->depth_keys64 = std::atoi(v) != 0;
   if (const char* v = std::getenv("GSR_BWRED")) c->bw_reduce = std::atoi(v);
   if (const char* v = std::getenv("GSR_K6ORDER")) c->k6_order = std::atoi(v) != 0;
+  if (const char* v = std::getenv("GSR_PACK")) c->pack_tile_keys = std::atoi(v);
   if (const char* v = std::getenv("GSR_TSORT"))
     c->tile_sort_mode = std::string(v) == "radix" ? 2 : (std::string(v) == "cs" ? 1 : 0);
   e = cudaMallocHost(&c->host_pinned, 4096);

@@ -810,13 +810,15 @@ __device__ __forceinline__ int owner_of(uint32_t excl, uint32_t j) {  // largest
   return s;
 }
 
-template <typename KeyT>
+template <typename KeyT, bool PACK>
 __global__ void __launch_bounds__(256) k3_emit(const KeyT* __restrict__ dkeys, const uint32_t* __restrict__ dvals,
                                                int64_t nvis, const uint4* __restrict__ span, int64_t n, uint32_t gx,
                                                uint32_t tpv, int W, uint32_t* __restrict__ tkeys,
                                                uint32_t* __restrict__ tvals, uint32_t* __restrict__ counts,
                                                uint64_t* __restrict__ lb, uint32_t* __restrict__ ctr,
-                                               int smem_bins, int vshift) {
+                                               int smem_bins, int vshift, int gbits) {
+  // gbits > 0: each key leaves as ONE packed word (tile within its view <<
+  // gbits | g) in tkeys and tvals is not written (the K4c path unpacks it)
   // Per-tile counts: a shared-memory histogram over the tiles of the block's
   // first view (a depth-sorted block almost always lies in one view), flushed
   // with one global atomic per non-empty bin; other views go straight to
@@ -897,7 +899,7 @@ __global__ void __launch_bounds__(256) k3_emit(const KeyT* __restrict__ dkeys, c
       const uint32_t oex = __shfl_sync(FULL, rexcl, s);
       const uint32_t og = __shfl_sync(FULL, g[r], s);
       const uint32_t ov = __shfl_sync(FULL, view[r], s);
-      uint32_t w = 0, kb = 0;
+      uint32_t w = 0, kb = 0, kl = 0;
       if (j < rtot) {
         const uint32_t py0 = opyr & 0xffffu, py1 = opyr >> 16;
         const uint32_t ty = (py0 >> 4) + (j - oex);
@@ -905,6 +907,7 @@ __global__ void __launch_bounds__(256) k3_emit(const KeyT* __restrict__ dkeys, c
         row_span(u, v, sp, sh, sic, sdys, py0, py1, ty, W, x0, x1);
         w = x1 - x0;
         kb = ov * tpv + ty * gx + x0;
+        kl = PACK ? ((ty * gx + x0) << gbits) | og : og;
       }
       const uint32_t winc = warp_incl_scan<uint32_t>(w);
       const uint32_t wexcl = winc - w;
@@ -914,11 +917,15 @@ __global__ void __launch_bounds__(256) k3_emit(const KeyT* __restrict__ dkeys, c
         const int t = owner_of(wexcl, k);
         const uint32_t okb = __shfl_sync(FULL, kb, t);
         const uint32_t owx = __shfl_sync(FULL, wexcl, t);
-        const uint32_t ogg = __shfl_sync(FULL, og, t);
+        const uint32_t okl = __shfl_sync(FULL, kl, t);
         if (k < wt) {
           const uint32_t key = okb + (k - owx);
-          tkeys[base + k] = key;
-          tvals[base + k] = ogg;
+          if (PACK) {
+            tkeys[base + k] = okl + ((k - owx) << gbits);
+          } else {
+            tkeys[base + k] = key;
+            tvals[base + k] = okl;
+          }
           if (key - lo < (uint32_t)smem_bins)
             atomicAdd(s_cnt + (key - lo), 1u);
           else
@@ -1053,7 +1060,7 @@ __global__ void __launch_bounds__(256) cs_meta(const uint2* __restrict__ ranges,
 }
 
 __global__ void __launch_bounds__(256) cs_hist(const uint32_t* __restrict__ tkeys, const uint32_t* __restrict__ meta,
-                                               int V, uint32_t tpv, uint32_t* __restrict__ H) {
+                                               int V, uint32_t tpv, uint32_t* __restrict__ H, int gbits) {
   extern __shared__ uint32_t s_h[];
   const uint32_t chunk = blockIdx.x;
   if (chunk >= meta[(V + 1) + V]) return;
@@ -1063,7 +1070,10 @@ __global__ void __launch_bounds__(256) cs_hist(const uint32_t* __restrict__ tkey
   for (uint32_t d = threadIdx.x; d < tpv; d += 256) s_h[d] = 0;
   __syncthreads();
   const uint32_t vb = (uint32_t)v * tpv;
-  for (uint32_t i = k0 + threadIdx.x; i < k1; i += 256) atomicAdd(s_h + (__ldg(tkeys + i) - vb), 1u);
+  if (gbits)
+    for (uint32_t i = k0 + threadIdx.x; i < k1; i += 256) atomicAdd(s_h + (__ldg(tkeys + i) >> gbits), 1u);
+  else
+    for (uint32_t i = k0 + threadIdx.x; i < k1; i += 256) atomicAdd(s_h + (__ldg(tkeys + i) - vb), 1u);
   __syncthreads();
   uint32_t* row = H + (size_t)chunk * tpv;
   for (uint32_t d = threadIdx.x; d < tpv; d += 256) row[d] = s_h[d];
@@ -1098,14 +1108,16 @@ __global__ void __launch_bounds__(256) cs_scan(const uint2* __restrict__ ranges,
   }
 }
 
-template <int W>
-__global__ void __launch_bounds__(W * 32) cs_scatter(const uint32_t* __restrict__ tkeys,
+template <int W, bool PACK>
+__global__ void __launch_bounds__(W * 32, 3) cs_scatter(const uint32_t* __restrict__ tkeys,
                                                      const uint32_t* __restrict__ tvals,
                                                      const uint32_t* __restrict__ meta, int V, uint32_t tpv,
                                                      int dbits, uint32_t tslice, int nslice,
                                                      const uint32_t* __restrict__ H,
                                                      uint32_t* __restrict__ vals_out, uint64_t* __restrict__ keys64,
-                                                     const uint32_t* __restrict__ depth_plane, int64_t nper) {
+                                                     const uint32_t* __restrict__ depth_plane, int64_t nper,
+                                                     int gbits) {
+  // gbits > 0: packed words (tile within the view << gbits | g), no tvals
   // shared memory: s_base [tpv] u32 (chunk offset + keys so far), s_sub [tpv]
   // u32 (this sub-round's base), s_wh [W][tpv] u16 (per-warp counts, then
   // the exclusive prefix over the warps)
@@ -1140,8 +1152,14 @@ __global__ void __launch_bounds__(W * 32) cs_scatter(const uint32_t* __restrict_
 #pragma unroll
     for (int k = 0; k < CS_KPT; ++k) {
       const uint32_t i = wb + k * 32 + lane;
-      dg[k] = i < k1 ? __ldg(tkeys + i) - vb : 0xffffffffu;  // out of the slice: >= tn
-      vv[k] = (i < k1 && dg[k] < tn) ? __ldg(tvals + i) : 0u;
+      if (PACK) {
+        const uint32_t wd = i < k1 ? __ldg(tkeys + i) : 0xffffffffu;
+        dg[k] = i < k1 ? (wd >> gbits) - tb : 0xffffffffu;  // out of the slice: >= tn
+        vv[k] = wd & ((1u << gbits) - 1u);
+      } else {
+        dg[k] = i < k1 ? __ldg(tkeys + i) - vb : 0xffffffffu;  // out of the slice: >= tn
+        vv[k] = (i < k1 && dg[k] < tn) ? __ldg(tvals + i) : 0u;
+      }
     }
     // warp-local stable ranks: lanes holding the same tile digit (ballots per bit)
 #pragma unroll
@@ -1648,20 +1666,29 @@ static gsr_status bin_sort_impl(gsr_ctx* ctx, const uint32_t* bin_rec, int64_t n
     if ((s = check_cuda(ctx, cudaGetLastError(), "depth sort")) != GSR_OK) return s;
   }
 
+  // K4c (counting scatter) unless the tile count is too large or the radix
+  // tile sort is forced; its keys travel packed (tile << gbits | g, one
+  // 4-B word per key instead of two) when both fit in 32 bits
+  const bool use_cs = ctx->tile_sort_mode != 2 && tpv <= (uint64_t)CS_MAX_TPV;
+  const int gbits = (use_cs && ctx->pack_tile_keys && bits_for(tpv) + std::max(1, bits_for(n)) <= 32)
+                        ? std::max(1, bits_for(n)) : 0;
+
   // ---- K3: emission + counts ----
   int sp = stage_begin(ctx, GSR_STAGE_EMIT, st);
   const int bins = tpv <= 12288 ? (int)tpv : 0;  // <= 48 KB of shared memory
   if (wide && !co)
-    k3_emit<uint64_t><<<(unsigned)nb3, 256, bins * 4, st>>>((const uint64_t*)ck, cvv, nvis, p_span, n, gx,
+    (gbits ? k3_emit<uint64_t, true> : k3_emit<uint64_t, false>)<<<(unsigned)nb3, 256, bins * 4, st>>>(
+        (const uint64_t*)ck, cvv, nvis, p_span, n, gx,
                                                             (uint32_t)tpv, W, (uint32_t*)tka, (uint32_t*)tva,
-                                                            (uint32_t*)cnt, lb3, ctrs + 5, bins, 32);
+                                                            (uint32_t*)cnt, lb3, ctrs + 5, bins, 32, gbits);
   else
-    k3_emit<uint32_t><<<(unsigned)nb3, 256, bins * 4, st>>>((const uint32_t*)ck, cvv, nvis, p_span, n, gx,
+    (gbits ? k3_emit<uint32_t, true> : k3_emit<uint32_t, false>)<<<(unsigned)nb3, 256, bins * 4, st>>>(
+        (const uint32_t*)ck, cvv, nvis, p_span, n, gx,
                                                             (uint32_t)tpv, W, (uint32_t*)tka, (uint32_t*)tva,
                                                             (uint32_t*)cnt, lb3, ctrs + 5, bins,
-                                                            co ? cshift : dshift);
+                                                            co ? cshift : dshift, gbits);
   stage_end(ctx, sp, st);
-  account(ctx, GSR_STAGE_EMIT, 1, 44.0 * nvis + 8.0 * K + 4.0 * T);
+  account(ctx, GSR_STAGE_EMIT, 1, 44.0 * nvis + (gbits ? 4.0 : 8.0) * K + 4.0 * T);
   if ((s = check_cuda(ctx, cudaGetLastError(), "k3_emit")) != GSR_OK) return s;
 
   // ---- K5: ranges + tile-sort histograms ----
@@ -1678,7 +1705,6 @@ static gsr_status bin_sort_impl(gsr_ctx* ctx, const uint32_t* bin_rec, int64_t n
   // (measured: c3 2,500 tiles 1.09 -> 0.79 ms per batch; c4 8,160 tiles in 2
   // slices 804 vs 799 views/s for the radix passes; unsliced with 4 warps 609).
   // GSR_TSORT=radix forces the two onesweep passes.
-  const bool use_cs = ctx->tile_sort_mode != 2 && tpv <= (uint64_t)CS_MAX_TPV;
   if (use_cs) {
     // K4c counting scatter (default)
     const uint64_t nchunks_max = (uint64_t)(K + CS_CHUNK - 1) / CS_CHUNK + (uint64_t)n_views;
@@ -1691,20 +1717,21 @@ static gsr_status bin_sort_impl(gsr_ctx* ctx, const uint32_t* bin_rec, int64_t n
     sp = stage_begin(ctx, GSR_STAGE_TILE_SORT, st);
     cs_meta<<<1, 32, 0, st>>>((const uint2*)ranges, n_views, (uint32_t)tpv, (uint32_t)K, (uint32_t*)meta);
     cs_hist<<<(unsigned)nchunks_max, 256, tpv * 4, st>>>((const uint32_t*)tka, (const uint32_t*)meta, n_views,
-                                                          (uint32_t)tpv, (uint32_t*)hm);
+                                                          (uint32_t)tpv, (uint32_t*)hm, gbits);
     cs_scan<<<(unsigned)((T + 255) / 256), 256, 0, st>>>((const uint2*)ranges, (const uint32_t*)meta, n_views,
                                                          (uint32_t)tpv, (uint32_t*)hm);
     const int dbits = std::max(1, bits_for(tslice));
-    cudaFuncSetAttribute(cs_scatter<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cs_scatter<8><<<(unsigned)(nchunks_max * nslice), 256, smem, st>>>(
+    auto scat = gbits ? cs_scatter<8, true> : cs_scatter<8, false>;
+    cudaFuncSetAttribute(scat, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    scat<<<(unsigned)(nchunks_max * nslice), 256, smem, st>>>(
         (const uint32_t*)tka, (const uint32_t*)tva, (const uint32_t*)meta, n_views, (uint32_t)tpv, dbits, tslice,
-        nslice, (const uint32_t*)hm, vals, keys, p_depth, n);
+        nslice, (const uint32_t*)hm, vals, keys, p_depth, n, gbits);
     stage_end(ctx, sp, st);
-    // hist reads 4 B/key; scatter reads 8 B/key and writes the 4-B values
-    // (+ 8-B keys when asked); the chunk x tile matrix is written, scanned in
-    // place and read once
+    // hist reads 4 B/key; scatter reads 8 B/key (4 B packed) and writes the
+    // 4-B values (+ 8-B keys when asked); the chunk x tile matrix is written,
+    // scanned in place and read once
     const double hbytes = (double)(K + CS_CHUNK - 1) / CS_CHUNK * (double)tpv * 4.0;
-    account(ctx, GSR_STAGE_TILE_SORT, 4, (16.0 + (keys ? 8.0 : 0.0)) * K + 4.0 * hbytes);
+    account(ctx, GSR_STAGE_TILE_SORT, 4, ((gbits ? 12.0 : 16.0) + (keys ? 8.0 : 0.0)) * K + 4.0 * hbytes);
     if ((s = check_cuda(ctx, cudaGetLastError(), "tile counting scatter")) != GSR_OK) return s;
   } else {
   sp = stage_begin(ctx, GSR_STAGE_TILE_SORT, st);

@@ -152,6 +152,7 @@ struct gsr_ctx {
   bool depth_keys64 = false;  // force the 64-bit depth-sort keys (GSR_DKEY64=1)
   int bw_reduce = 2;          // K6b warp reduction: 0 shuffle trees, 1 smem atomics, 2 butterfly (GSR_BWRED)
   bool k6_order = false;      // K6 largest-tile-first launch order (GSR_K6ORDER=1)
+  int pack_tile_keys = 1;     // K3 -> K4c keys as one (tile << gbits | g) word when they fit (GSR_PACK=0: two planes)
   int tile_sort_mode = 0;     // 0 / 1: K4c counting scatter up to 12,288 tiles per view, 2: K4b radix (GSR_TSORT=radix)
   int composite_variant = 8;  // K6: 1 block-sync LDG, 2 TMA bulk/record, 3 TMA gather4, 4 cp.async, 5 warp-independent LDG, 6 = 5 + exact ellipse-box cull, 7 = 6 with per-warp TMA gather4 buffers (GSR_STAGES: 2 or 4), 8 = 6 with compacted hit staging + counted hit loop (default)
 };

@@ -233,7 +233,7 @@ def test_depth_key_widths(ctx):
 
 @pytest.mark.parametrize("env", ["GSR_COMPOSITE=1", "GSR_COMPOSITE=6", "GSR_COMPOSITE=2", "GSR_COMPOSITE=3", "GSR_COMPOSITE=4",
                                  "GSR_COMPOSITE=5", "GSR_COMPOSITE=7", "GSR_COMPOSITE=7 GSR_STAGES=2", "GSR_K6ORDER=1",  "GSR_COMPOSITE=3 GSR_STAGES=8", "GSR_COMPOSITE=3 GSR_PIX=2",
-                                 "GSR_SORT=2", "GSR_SORT=3", "GSR_KPT=8", "GSR_TSORT=radix", "GSR_TSORT=cs",
+                                 "GSR_SORT=2", "GSR_SORT=3", "GSR_KPT=8", "GSR_TSORT=radix", "GSR_TSORT=cs", "GSR_PACK=0",
                                  "GSR_TSORT=radix GSR_SORT=2"])
 def test_measured_variants_stay_exact(env, monkeypatch):
     """Every A/B variant DESIGN.md reports a measurement for (K6 loaders: block-
@@ -252,7 +252,8 @@ def test_measured_variants_stay_exact(env, monkeypatch):
     assert np.array_equal(g["rgbu"], o["rgbu"])
 
 
-@pytest.mark.parametrize("W,H,env", [(1200, 1000, ""), (1200, 1000, "GSR_TSORT=radix"), (1800, 1760, "")])
+@pytest.mark.parametrize("W,H,env", [(1200, 1000, ""), (1200, 1000, "GSR_PACK=0"), (1200, 1000, "GSR_TSORT=radix"),
+                                     (1800, 1760, "")])
 def test_large_tile_counts(W, H, env, monkeypatch):
     """Tile counts past the K4c slice size (4,352 tiles: 75 x 63 = 4,725 tiles
     in 2 slices; and the same through the radix passes) and past the
