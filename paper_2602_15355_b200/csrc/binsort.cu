@@ -943,6 +943,59 @@ __global__ void __launch_bounds__(256) k3_emit(const KeyT* __restrict__ dkeys, c
 }
 
 // ---------------------------------------------------------------------------
+// K5 (K4c path): ranges[t] = [s, s + counts[t]), s = exclusive prefix of
+// counts, as a single-pass decoupled look-back scan over 256-thread blocks of
+// 16 consecutive tiles per thread (small blocks: the sort stream's kernels
+// must find room on SMs the other slot's composite occupies; the one-block
+// K5 below waited for a whole SM).
+constexpr int K5_ITEMS = 16;
+constexpr int K5_TILE = 256 * K5_ITEMS;
+
+__global__ void __launch_bounds__(256) k5_scan(const uint32_t* __restrict__ counts, int64_t T,
+                                               uint2* __restrict__ ranges, uint64_t* __restrict__ lb,
+                                               uint32_t* __restrict__ ctr) {
+  __shared__ uint32_t s_w[8];
+  __shared__ uint32_t s_bid, s_prefix;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) s_bid = atomicAdd(ctr, 1u);
+  __syncthreads();
+  const int64_t bid = s_bid;
+  const int64_t t0 = bid * K5_TILE + (int64_t)tid * K5_ITEMS;
+  uint32_t v[K5_ITEMS];
+  uint32_t sum = 0;
+#pragma unroll
+  for (int k = 0; k < K5_ITEMS; ++k) {
+    v[k] = t0 + k < T ? __ldg(counts + t0 + k) : 0u;
+    sum += v[k];
+  }
+  const uint32_t inc = warp_incl_scan<uint32_t>(sum);
+  if (lane == 31) s_w[warp] = inc;
+  __syncthreads();
+  if (warp == 0) {
+    const uint32_t wv = lane < 8 ? s_w[lane] : 0u;
+    const uint32_t wi = warp_incl_scan<uint32_t>(wv);
+    const uint32_t tot = __shfl_sync(FULL, wi, 7);
+    if (lane < 8) s_w[lane] = wi - wv;
+    uint64_t p = 0;
+    if (bid == 0) {
+      if (lane == 0) publish(lb, 0, LB_INC | tot);
+    } else {
+      if (lane == 0) publish(lb, bid, LB_AGG | tot);
+      p = warp_lookback(lb, bid);
+      if (lane == 0) publish(lb, bid, LB_INC | (p + tot));
+    }
+    if (lane == 0) s_prefix = (uint32_t)p;
+  }
+  __syncthreads();
+  uint32_t run = s_prefix + s_w[warp] + inc - sum;
+#pragma unroll
+  for (int k = 0; k < K5_ITEMS; ++k) {
+    if (t0 + k < T) ranges[t0 + k] = make_uint2(run, run + v[k]);
+    run += v[k];
+  }
+}
+
+// ---------------------------------------------------------------------------
 // K5: ranges[t] = [s, s + counts[t]) with s = exclusive prefix of counts, and
 // the tile-sort digit histograms + bases.  One block of 1024 threads.
 __global__ void __launch_bounds__(1024) k5_ranges(const uint32_t* __restrict__ counts, int64_t T,
@@ -1628,7 +1681,9 @@ static gsr_status bin_sort_impl(gsr_ctx* ctx, const uint32_t* bin_rec, int64_t n
   const size_t o_d = 0;
   const size_t o_3 = align_up(o_d + dpasses * nbd * 256 * 4);
   const size_t o_t = align_up(o_3 + nb3 * 8);
-  const size_t o_c = align_up(o_t + tpasses * nbt * 256 * 4);
+  const size_t nb5 = (size_t)((T + K5_TILE - 1) / K5_TILE);
+  const size_t o_5 = align_up(o_t + tpasses * nbt * 256 * 4);
+  const size_t o_c = align_up(o_5 + nb5 * 8);
   const size_t lb2 = o_c + 64 * 4;
   // K2's look-back words are dead now (the sync above ordered them): reuse the slot.
   if ((s = ensure(ctx, S_LOOKBACK, lb2, &lb)) != GSR_OK) return s;
@@ -1637,7 +1692,8 @@ static gsr_status bin_sort_impl(gsr_ctx* ctx, const uint32_t* bin_rec, int64_t n
   uint32_t* lbd = (uint32_t*)((char*)lb + o_d);
   uint64_t* lb3 = (uint64_t*)((char*)lb + o_3);
   uint32_t* lbt = (uint32_t*)((char*)lb + o_t);
-  uint32_t* ctrs = (uint32_t*)((char*)lb + o_c);  // [0..4] depth, [5] k3, [6..9] tile
+  uint64_t* lb5 = (uint64_t*)((char*)lb + o_5);
+  uint32_t* ctrs = (uint32_t*)((char*)lb + o_c);  // [0..4] depth, [5] k3, [6..9] tile, [10] k5
 
   // ---- K4a: depth sort of the visible pairs (skipped in the cached order) ----
   const void* ck = dka;
@@ -1693,7 +1749,11 @@ static gsr_status bin_sort_impl(gsr_ctx* ctx, const uint32_t* bin_rec, int64_t n
 
   // ---- K5: ranges + tile-sort histograms ----
   sp = stage_begin(ctx, GSR_STAGE_RANGES, st);
-  k5_ranges<<<1, 1024, 0, st>>>((const uint32_t*)cnt, (int64_t)T, (uint2*)ranges, tpasses, thist, tbase);
+  // (the K4b radix passes also need the tile-digit histograms: one block)
+  if (use_cs)
+    k5_scan<<<(unsigned)nb5, 256, 0, st>>>((const uint32_t*)cnt, (int64_t)T, (uint2*)ranges, lb5, ctrs + 10);
+  else
+    k5_ranges<<<1, 1024, 0, st>>>((const uint32_t*)cnt, (int64_t)T, (uint2*)ranges, tpasses, thist, tbase);
   stage_end(ctx, sp, st);
   account(ctx, GSR_STAGE_RANGES, 1, 12.0 * T);
   if ((s = check_cuda(ctx, cudaGetLastError(), "k5_ranges")) != GSR_OK) return s;
