@@ -1,5 +1,5 @@
 """Parity at BASELINE.json's full sizes, in the launch configuration bench.py
-times (ViewScorer, 16-view batches), on sampled views the oracle can render
+times (ViewScorer; c3 in bench.py's 32-view batches), on sampled views the oracle can render
 (one view per host thread).  Bar: images <= 1e-4 abs per channel, scores
 <= 1e-4 relative, same NBV over the sample unless the top-2 tie within 1e-4."""
 import os
@@ -34,8 +34,8 @@ def _gpu_images(field, cams, batch_views=16):
     return np.concatenate(out_img), np.concatenate(out_sc), sc
 
 
-def _check(field, cams, tag):
-    img, sc, scorer = _gpu_images(field, cams)
+def _check(field, cams, tag, batch_views=16):
+    img, sc, scorer = _gpu_images(field, cams, batch_views)
     ref, _, _, rimg = oracle.render_views(field, cams, n_threads=THREADS, images=True)
     d = np.abs(img.astype(np.float64) - rimg)
     assert d.max() <= 1e-4, (tag, d.max())
@@ -47,12 +47,12 @@ def _check(field, cams, tag):
 
 
 def test_config3_sampled_views_full_size():
-    """configs[2]: 1M Gaussians, 800x800, f = 900; 16 strided views of the 1,024,
-    one 16-view batch (the bench's batch size); then the scores of the same
+    """configs[2]: 1M Gaussians, 800x800, f = 900; 32 strided views of the 1,024,
+    one 32-view batch (the bench's batch size); then the scores of the same
     views inside a full 1,024-view scoring pass are bit-identical."""
     scene = synth.make_scene(3)
-    idx = np.linspace(0, 1023, 16).round().astype(np.int64)
-    img, sc, scorer = _check(scene.field, scene.cameras[idx], "c3")
+    idx = np.linspace(0, 1023, 32).round().astype(np.int64)
+    img, sc, scorer = _check(scene.field, scene.cameras[idx], "c3", batch_views=32)
     full = scorer.score_views(scene.cameras).cpu().numpy()
     assert np.array_equal(full[idx], sc)
     assert np.all(np.isfinite(full)) and np.all(full >= 0)
