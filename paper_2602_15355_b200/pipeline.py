@@ -265,13 +265,21 @@ class Renderer:
         V, n = len(cams), self.field.n
         W, H = int(cams[0]["width"]), int(cams[0]["height"])
         T = V * tiles_per_view(cams[0])
-        self.rec = torch.empty((V, max(n, 1), 12), dtype=torch.float32, device=self.dev)
-        self.bin = torch.empty(10 * V * max(n, 1), dtype=torch.int32, device=self.dev)
-        self.ranges = torch.empty((T, 2), dtype=torch.int32, device=self.dev)
+        # buffers are reused while the batch shape stays the same (a caller
+        # holding the previous image must copy it first)
+        shape = (V, n, W, H)
+        if getattr(self, "_shape", None) != shape:
+            self.rec = torch.empty((V, max(n, 1), 12), dtype=torch.float32, device=self.dev)
+            self.bin = torch.empty(10 * V * max(n, 1), dtype=torch.int32, device=self.dev)
+            self.ranges = torch.empty((T, 2), dtype=torch.int32, device=self.dev)
+            self.partial = torch.empty(T, dtype=torch.float32, device=self.dev)
+            self.rgbu = torch.empty((V, H, W, 4), dtype=torch.float32, device=self.dev)
+            self._shape = shape
         gsr.gsr_project(self.ctx, self.field, cams, self.rec, self.bin, stream, lod=self.lod)
         cap = getattr(self, "_cap", 1 << 20)
         while True:
-            self.vals = torch.empty(cap, dtype=torch.int32, device=self.dev)
+            if getattr(self, "vals", None) is None or self.vals.numel() < cap:
+                self.vals = torch.empty(cap, dtype=torch.int32, device=self.dev)
             try:
                 gsr.gsr_bin_sort(self.ctx, self.bin, n, cams, self.vals, cap, self.ranges, stream=stream)
                 break
@@ -280,8 +288,6 @@ class Renderer:
                     raise
                 cap = int(math.ceil(e.required * 1.25)) + 1024
         self._cap = cap
-        self.partial = torch.empty(T, dtype=torch.float32, device=self.dev)
-        self.rgbu = torch.empty((V, H, W, 4), dtype=torch.float32, device=self.dev)
         gsr.gsr_composite(self.ctx, self.rec, n, self.vals, self.ranges, cams, self.partial, rgbu=self.rgbu,
                           stream=stream)
         self._cams = cams
