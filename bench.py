@@ -527,6 +527,7 @@ def main():
     roof = {"bound": "alu", "kernel": "k6_composite", "achieved": round(ach_ops, 2), "peak": round(peak_ops, 2),
             "unit": "Top/s", "frac": round(ach_ops / peak_ops, 4),
             "traffic": traffic.get("k6_composite"),
+            "ncu": traffic.get("k6_ncu"),  # FP32-pipe and shared-memory fractions (north_star), committed capture
             "work": "28 FP32 ops per (pixel, list entry) pair the plain definition evaluates + 8 per blended "
                     f"fragment, per launch = {args.batch_views} views",
             "peak_source": f"148 SMs x 128 FP32 lanes x {f_clk / 1e6:.0f} MHz (median SM clock under load)",
