@@ -1731,18 +1731,20 @@ static gsr_status bin_sort_impl(gsr_ctx* ctx, const uint32_t* bin_rec, int64_t n
 
   // ---- K3: emission + counts ----
   int sp = stage_begin(ctx, GSR_STAGE_EMIT, st);
-  const int bins = tpv <= 12288 ? (int)tpv : 0;  // <= 48 KB of shared memory
-  if (wide && !co)
-    (gbits ? k3_emit<uint64_t, true> : k3_emit<uint64_t, false>)<<<(unsigned)nb3, 256, bins * 4, st>>>(
-        (const uint64_t*)ck, cvv, nvis, p_span, n, gx,
-                                                            (uint32_t)tpv, W, (uint32_t*)tka, (uint32_t*)tva,
-                                                            (uint32_t*)cnt, lb3, ctrs + 5, bins, 32, gbits);
-  else
-    (gbits ? k3_emit<uint32_t, true> : k3_emit<uint32_t, false>)<<<(unsigned)nb3, 256, bins * 4, st>>>(
-        (const uint32_t*)ck, cvv, nvis, p_span, n, gx,
-                                                            (uint32_t)tpv, W, (uint32_t*)tka, (uint32_t*)tva,
-                                                            (uint32_t*)cnt, lb3, ctrs + 5, bins,
-                                                            co ? cshift : dshift, gbits);
+  const int bins = tpv <= 12288 ? (int)tpv : 0;  // <= 48 KB of dynamic shared memory (opt-in above 48 KB total)
+  if (wide && !co) {
+    auto k3 = gbits ? k3_emit<uint64_t, true> : k3_emit<uint64_t, false>;
+    cudaFuncSetAttribute(k3, cudaFuncAttributeMaxDynamicSharedMemorySize, bins * 4);
+    k3<<<(unsigned)nb3, 256, bins * 4, st>>>((const uint64_t*)ck, cvv, nvis, p_span, n, gx, (uint32_t)tpv, W,
+                                             (uint32_t*)tka, (uint32_t*)tva, (uint32_t*)cnt, lb3, ctrs + 5, bins,
+                                             32, gbits);
+  } else {
+    auto k3 = gbits ? k3_emit<uint32_t, true> : k3_emit<uint32_t, false>;
+    cudaFuncSetAttribute(k3, cudaFuncAttributeMaxDynamicSharedMemorySize, bins * 4);
+    k3<<<(unsigned)nb3, 256, bins * 4, st>>>((const uint32_t*)ck, cvv, nvis, p_span, n, gx, (uint32_t)tpv, W,
+                                             (uint32_t*)tka, (uint32_t*)tva, (uint32_t*)cnt, lb3, ctrs + 5, bins,
+                                             co ? cshift : dshift, gbits);
+  }
   stage_end(ctx, sp, st);
   account(ctx, GSR_STAGE_EMIT, 1, 44.0 * nvis + (gbits ? 4.0 : 8.0) * K + 4.0 * T);
   if ((s = check_cuda(ctx, cudaGetLastError(), "k3_emit")) != GSR_OK) return s;

@@ -253,7 +253,7 @@ def test_measured_variants_stay_exact(env, monkeypatch):
 
 
 @pytest.mark.parametrize("W,H,env", [(1200, 1000, ""), (1200, 1000, "GSR_PACK=0"), (1200, 1000, "GSR_TSORT=radix"),
-                                     (1800, 1760, "")])
+                                     (1760, 1760, ""), (1800, 1760, "")])
 def test_large_tile_counts(W, H, env, monkeypatch):
     """Tile counts past the K4c slice size (4,352 tiles: 75 x 63 = 4,725 tiles
     in 2 slices; and the same through the radix passes) and past the
