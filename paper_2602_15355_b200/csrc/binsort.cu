@@ -1074,10 +1074,14 @@ __global__ void __launch_bounds__(1024) k5_ranges(const uint32_t* __restrict__ c
 //            stable ranks (ballot match on the tile digit), exclusive prefix
 //            over the warps, plus the chunk's running per-tile counter; the
 //            value goes straight to its final slot.
-// DRAM traffic per key: 4 B (hist) + 8 B read + 4 B write (scatter) + the
-// H matrix (CS_CHUNK = 16 K keys: ~1 B/key), vs 28 B/key for two passes.
+// DRAM traffic per key: 4 B (hist) + 4 B (packed) or 8 B read + 4 B write
+// (scatter) + the H matrix (CS_CHUNK = 64 K keys: ~0.15 B/key at c3), vs
+// 28 B/key for two radix passes.
 constexpr int CS_KPT = 8;
-constexpr int CS_CHUNK = 32768;
+#ifndef CS_CHUNK_KEYS
+#define CS_CHUNK_KEYS 65536  // measured: 64 K 2,895, 32 K 2,887, 16 K 2,880 views/s
+#endif
+constexpr int CS_CHUNK = CS_CHUNK_KEYS;
 constexpr int CS_MAX_TPV = 12288;
 constexpr int CS_AUTO_TPV = 4352;
 
