@@ -87,6 +87,25 @@ def test_batch_size_invariance_and_determinism(ctx):
             assert np.array_equal(part["scores"], full["scores"][b0:b0 + len(cams)])
 
 
+def test_maximum_batch_64_views(ctx):
+    """GSR_MAX_VIEWS = 64 views in one batch (6 view bits in the depth keys):
+    bit-exact against the oracle, and the same per-view outputs as 8-view
+    batches; ViewScorer with 64-view batches gives the same scores."""
+    from paper_2602_15355_b200 import Gaussians
+    from paper_2602_15355_b200.pipeline import ViewScorer
+    import torch
+    sc = synth.make_scene(1, n_override=3000, views=64)
+    g, _ = _full_check(ctx, sc.field, sc.cameras)
+    assert np.array_equal(g["rgbu"], oracle_batch(sc.field, sc.cameras)["rgbu"])
+    for b0 in (0, 56):
+        part = gpu_batch(ctx, sc.field, sc.cameras[b0:b0 + 8])
+        assert np.array_equal(part["rgbu"], g["rgbu"][b0:b0 + 8])
+        assert np.array_equal(part["scores"], g["scores"][b0:b0 + 8])
+    G = Gaussians(torch.from_numpy(sc.field.planes).cuda(), sc.field.sh_degree)
+    s64 = ViewScorer(G, batch_views=64).score_views(sc.cameras).cpu().numpy()
+    assert np.array_equal(s64, g["scores"])
+
+
 def test_uncertainty_scaling_doubles_scores(ctx):
     sc = synth.make_scene(1, n_override=4000, views=4)
     a = gpu_batch(ctx, sc.field, sc.cameras, want_unsorted=False)
