@@ -545,7 +545,7 @@ def main():
 
     # the same K6 roofline with K6 alone on the GPU (one slot, one step): the
     # two-stream spans above include time the composite shares with the sorts
-    iso = None
+    iso = iso_sort = None
     if not args.no_extras and world == 1:
         iso_scorer = ViewScorer(G, batch_views=args.batch_views, n_slots=1)
         iso_scorer.score_views(cams)
@@ -563,6 +563,12 @@ def main():
                "peak": round(peak_ops, 2), "unit": "Top/s", "frac": round(iso_ops / peak_ops, 4),
                "ms_per_step": round(ist["composite"]["ms"], 2),
                "share_of_serial_step": round(ist["composite"]["ms"] / sum(v["ms"] for v in ist.values()), 3)}
+        # the key sort alone too (one stream: no SMs shared with a composite)
+        iso_sort_gbs = ist["tile_sort"]["bytes"] / (ist["tile_sort"]["ms"] / 1e3) / 1e9
+        iso_sort = {"bound": "hbm", "kernel": "tile_sort (one stream)", "achieved": round(iso_sort_gbs, 1),
+                    "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": round(iso_sort_gbs / peaks["hbm_gbs"], 4),
+                    "ms_per_step": round(ist["tile_sort"]["ms"], 2),
+                    "share_of_serial_step": round(ist["tile_sort"]["ms"] / sum(v["ms"] for v in ist.values()), 3)}
         iso_scorer.timing(False)
         del iso_scorer
         torch.cuda.empty_cache()
@@ -599,7 +605,7 @@ def main():
             "data": "synthetic (seeded generator of BASELINE.json configs[2]; no dataset)",
             "config": cfg_json, "fragments_per_sec": frag_per_s, "evaluated_pairs_per_sec": eval_per_s,
             "wall_ms_per_step": round(wall_ms / args.steps, 3), "roofline": roof, "roofline_isolated": iso,
-            "roofline_sort": roof_sort,
+            "roofline_sort": roof_sort, "roofline_sort_isolated": iso_sort,
             "stages": stage_tab,
             "gpu_launches": int(launches * world), "clocks": clk, "e2e": e2e, "collectives": coll,
             "keys_per_step_rank0": int(sum(scorer.last_keys))}
