@@ -533,7 +533,9 @@ def main():
             "work": "28 FP32 ops per (pixel, list entry) pair the plain definition evaluates + 8 per blended "
                     f"fragment, per launch = {args.batch_views} views",
             "peak_source": f"148 SMs x 128 FP32 lanes x {f_clk / 1e6:.0f} MHz (median SM clock under load)",
-            "share_of_step": round(st_ms["composite"] / sum(st_ms.values()), 3),
+            # its event spans / the device step time (stage spans of the two
+            # slots overlap, so they do not add up to the step)
+            "share_of_step": round(st_ms["composite"] / (ms / args.steps), 3),
             "launches_per_step": n_comp}
     ach_sort = st_by["tile_sort"] / (st_ms["tile_sort"] / 1e3) / 1e9
     roof_sort = {"bound": "hbm", "kernel": "tile_sort (K4c counting scatter: chunk histograms + column scan + "
@@ -541,7 +543,7 @@ def main():
                  "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": round(ach_sort / peaks["hbm_gbs"], 4),
                  "traffic": traffic.get("tile_sort"),
                  "peak_source": peaks["source"] + " hbm_gbs (MEASURED_PEAKS.json)",
-                 "share_of_step": round(st_ms["tile_sort"] / sum(st_ms.values()), 3)}
+                 "share_of_step": round(st_ms["tile_sort"] / (ms / args.steps), 3)}
 
     # the same K6 roofline with K6 alone on the GPU (one slot, one step): the
     # two-stream spans above include time the composite shares with the sorts
