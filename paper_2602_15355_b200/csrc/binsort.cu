@@ -1203,6 +1203,16 @@ __global__ void __launch_bounds__(W * 32, 3) cs_scatter(const uint32_t* __restri
   const uint32_t lt = (1u << lane) - 1u;
   uint16_t* wh = s_wh + (size_t)warp * ts;
   constexpr uint32_t SUB = W * 32 * CS_KPT;
+  // packed words of the next sub-round are loaded during this one's prefix
+  // and scatter (measured +0.15 %; the two-plane layout loads in place)
+  uint32_t nw[CS_KPT];
+  if (PACK) {
+#pragma unroll
+    for (int k = 0; k < CS_KPT; ++k) {
+      const uint32_t i = k0 + (uint32_t)warp * (32 * CS_KPT) + k * 32 + lane;
+      nw[k] = i < k1 ? __ldg(tkeys + i) : 0xffffffffu;
+    }
+  }
   for (uint32_t s0 = k0; s0 < k1; s0 += SUB) {
     const uint32_t wb = s0 + (uint32_t)warp * (32 * CS_KPT);
     uint32_t dg[CS_KPT], vv[CS_KPT], rk[CS_KPT];
@@ -1210,7 +1220,7 @@ __global__ void __launch_bounds__(W * 32, 3) cs_scatter(const uint32_t* __restri
     for (int k = 0; k < CS_KPT; ++k) {
       const uint32_t i = wb + k * 32 + lane;
       if (PACK) {
-        const uint32_t wd = i < k1 ? __ldg(tkeys + i) : 0xffffffffu;
+        const uint32_t wd = nw[k];
         dg[k] = i < k1 ? (wd >> gbits) - tb : 0xffffffffu;  // out of the slice: >= tn
         vv[k] = wd & ((1u << gbits) - 1u);
       } else {
@@ -1234,6 +1244,13 @@ __global__ void __launch_bounds__(W * 32, 3) cs_scatter(const uint32_t* __restri
       if (ok && (peers & lt) == 0) wh[dg[k]] = (uint16_t)(pre + __popc(peers));
       __syncwarp();
       rk[k] = pre + __popc(peers & lt);
+    }
+    if (PACK) {
+#pragma unroll
+      for (int k = 0; k < CS_KPT; ++k) {
+        const uint32_t i = wb + SUB + k * 32 + lane;
+        nw[k] = i < k1 ? __ldg(tkeys + i) : 0xffffffffu;
+      }
     }
     __syncthreads();
     // exclusive prefix over the warps, two tiles per 32-bit word (no carry:
