@@ -121,6 +121,7 @@ enum Slot {
   S_GRAD2D,                                 // NEXT-3 per-(view, g) 2D gradients
   S_CSH, S_CSMETA,                          // K4c chunk x tile offsets, view / chunk table
   S_K6ORDER,                                // K6 launch order (largest tiles first)
+  S_K6PART,                                 // K6 sub-tile block partial sums (variants 9-11)
   S_OPTIM,                                  // NEXT-3 loss partial sums
   S_NSLOTS
 };
@@ -154,7 +155,7 @@ struct gsr_ctx {
   bool k6_order = false;      // K6 largest-tile-first launch order (GSR_K6ORDER=1)
   int pack_tile_keys = 1;     // K3 -> K4c keys as one (tile << gbits | g) word when they fit (GSR_PACK=0: two planes)
   int tile_sort_mode = 0;     // 0 / 1: K4c counting scatter up to 12,288 tiles per view, 2: K4b radix (GSR_TSORT=radix)
-  int composite_variant = 8;  // K6: 1 block-sync LDG, 2 TMA bulk/record, 3 TMA gather4, 4 cp.async, 5 warp-independent LDG, 6 = 5 + exact ellipse-box cull, 7 = 6 with per-warp TMA gather4 buffers (GSR_STAGES: 2 or 4), 8 = 6 with compacted hit staging + counted hit loop (default)
+  int composite_variant = 10; // K6: 1 block-sync LDG, 2 TMA bulk/record, 3 TMA gather4, 4 cp.async, 5 warp-independent LDG, 6 = 5 + exact ellipse-box cull, 7 = 6 with per-warp TMA gather4 buffers (GSR_STAGES: 2 or 4), 8 = 6 with compacted hit staging + counted hit loop, 9 / 10 / 11 = 8 in blocks of 4 / 2 / 1 warps on part of a tile (10 default)
 };
 
 namespace gsr {

@@ -250,7 +250,7 @@ def test_depth_key_widths(ctx):
     _full_check(ctx, fld.subset(np.arange(n - 3)), cams64)  # fits: 32-bit keys
 
 
-@pytest.mark.parametrize("env", ["GSR_COMPOSITE=1", "GSR_COMPOSITE=6", "GSR_COMPOSITE=2", "GSR_COMPOSITE=3", "GSR_COMPOSITE=4",
+@pytest.mark.parametrize("env", ["GSR_COMPOSITE=1", "GSR_COMPOSITE=6", "GSR_COMPOSITE=8", "GSR_COMPOSITE=9", "GSR_COMPOSITE=11", "GSR_COMPOSITE=2", "GSR_COMPOSITE=3", "GSR_COMPOSITE=4",
                                  "GSR_COMPOSITE=5", "GSR_COMPOSITE=7", "GSR_COMPOSITE=7 GSR_STAGES=2", "GSR_K6ORDER=1",  "GSR_COMPOSITE=3 GSR_STAGES=8", "GSR_COMPOSITE=3 GSR_PIX=2",
                                  "GSR_SORT=2", "GSR_SORT=3", "GSR_KPT=8", "GSR_TSORT=radix", "GSR_TSORT=cs", "GSR_PACK=0",
                                  "GSR_TSORT=radix GSR_SORT=2"])
