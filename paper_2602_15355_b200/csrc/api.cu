@@ -85,6 +85,7 @@ gsr_status gsr_create(gsr_ctx** out, int device) {
   if (const char* v = std::getenv("GSR_KPT")) c->sort_kpt32 = std::atoi(v);
   if (const char* v = std::getenv("GSR_DKEY64")) c->depth_keys64 = std::atoi(v) != 0;
   if (const char* v = std::getenv("GSR_BWRED")) c->bw_reduce = std::atoi(v);
+  if (const char* v = std::getenv("GSR_BWNW")) c->bw_warps = std::atoi(v);
   if (const char* v = std::getenv("GSR_K6ORDER")) c->k6_order = std::atoi(v) != 0;
   if (const char* v = std::getenv("GSR_PACK")) c->pack_tile_keys = std::atoi(v);
   if (const char* v = std::getenv("GSR_TSORT"))

@@ -151,6 +151,7 @@ struct gsr_ctx {
   int composite_stages = 4;   // K6 ring depth (GSR_STAGES: 4 or 8)
   int composite_pix = 1;      // K6 pixels per consumer lane (GSR_PIX: 1 or 2)
   bool depth_keys64 = false;  // force the 64-bit depth-sort keys (GSR_DKEY64=1)
+  int bw_warps = 2;           // K6b warps per block: 2 (sub-tile blocks) or 8 (GSR_BWNW)
   int bw_reduce = 2;          // K6b warp reduction: 0 shuffle trees, 1 smem atomics, 2 butterfly (GSR_BWRED)
   bool k6_order = false;      // K6 largest-tile-first launch order (GSR_K6ORDER=1)
   int pack_tile_keys = 1;     // K3 -> K4c keys as one (tile << gbits | g) word when they fit (GSR_PACK=0: two planes)

@@ -80,12 +80,17 @@ def test_renderer_api_matches_oracle(ctx):
     _compare(got, bw.backward_views(fld, cams, G), 3)
 
 
-@pytest.mark.parametrize("red", ["0", "2"])
+@pytest.mark.parametrize("red", ["0", "2", "2 GSR_BWNW=8"])
 def test_backward_reduction_variants(ctx, red, monkeypatch):
     """K6b's warp reductions (shuffle trees / transposed butterfly, GSR_BWRED)
-    give the same gradients within the float tolerance."""
+    and block shapes (2-warp sub-tile blocks / one 8-warp block per tile,
+    GSR_BWNW) give the same gradients within the float tolerance."""
     from paper_2602_15355_b200 import Context
+    red, *extra = red.split()
     monkeypatch.setenv("GSR_BWRED", red)
+    for kv in extra:
+        k, v = kv.split("=")
+        monkeypatch.setenv(k, v)
     c = Context(0)
     fld, cams = synth.random_scene_small(8, 150, 40, 33, 40.0, 2, 2, logscale_mu=-2.4)
     G = np.random.default_rng(9).normal(size=(2, 33, 40, 4)).astype(np.float32)
