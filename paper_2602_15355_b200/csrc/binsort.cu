@@ -138,7 +138,10 @@ constexpr int K2_TILE = 256 * K2_ITEMS;
 // Same order either way; the 32-bit keys halve the depth sort's traffic
 // (4 passes x 8 B instead of 5 x 12 B per visible pair).
 template <typename KeyT>
-__global__ void __launch_bounds__(256) k2_compact(const uint32_t* __restrict__ depth_plane,
+#ifndef K2_MINB
+#define K2_MINB 5  // measured: 5 blocks (48 regs) 3,019, 4 (64) 3,014, unbounded (80) 3,001 views/s
+#endif
+__global__ void __launch_bounds__(256, K2_MINB) k2_compact(const uint32_t* __restrict__ depth_plane,
                                                   const uint32_t* __restrict__ nt_plane, int64_t M, int64_t n,
                                                   KeyT* __restrict__ dkeys, uint32_t* __restrict__ dvals,
                                                   uint32_t* __restrict__ emit_off, uint64_t* __restrict__ lb_vis,
