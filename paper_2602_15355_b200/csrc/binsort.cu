@@ -291,8 +291,11 @@ __global__ void __launch_bounds__(256) hist_u64(const uint64_t* __restrict__ key
 //         dynamic block ids).  LB = 1: the per-(digit, tile) output offsets were
 //         precomputed by rs_upsweep + rs_scan (lookback = gofs[256][ntiles]),
 //         so a tile needs no inter-block communication at all.
+#ifndef OS_MINB12
+#define OS_MINB12 4  // 12-key tiles: 4 blocks per SM (64 registers, small spills) measured +0.4 % over 3
+#endif
 template <typename KeyT, int KPT, int MODE, int LB = 0>
-__global__ void __launch_bounds__(256, (KPT <= 8 ? 4 : 3)) onesweep(const KeyT* __restrict__ kin, const uint32_t* __restrict__ vin,
+__global__ void __launch_bounds__(256, (KPT <= 8 ? 4 : OS_MINB12)) onesweep(const KeyT* __restrict__ kin, const uint32_t* __restrict__ vin,
                                                 KeyT* __restrict__ kout, uint32_t* __restrict__ vout, uint32_t n,
                                                 int shift, int nbits, const uint32_t* __restrict__ base,
                                                 uint32_t* __restrict__ lookback, uint32_t* __restrict__ ctr,
@@ -814,7 +817,10 @@ __device__ __forceinline__ int owner_of(uint32_t excl, uint32_t j) {  // largest
 }
 
 template <typename KeyT, bool PACK>
-__global__ void __launch_bounds__(256) k3_emit(const KeyT* __restrict__ dkeys, const uint32_t* __restrict__ dvals,
+#ifndef K3_MINB
+#define K3_MINB 6  // measured (with OS_MINB12 4): 6 blocks 3,076, 5 3,052, 8 3,059, unbounded (64 regs) 3,019 views/s
+#endif
+__global__ void __launch_bounds__(256, K3_MINB) k3_emit(const KeyT* __restrict__ dkeys, const uint32_t* __restrict__ dvals,
                                                int64_t nvis, const uint4* __restrict__ span, int64_t n, uint32_t gx,
                                                uint32_t tpv, int W, uint32_t* __restrict__ tkeys,
                                                uint32_t* __restrict__ tvals, uint32_t* __restrict__ counts,
