@@ -43,9 +43,8 @@ def parse():
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="gsr", choices=["gsr", "reference"])
     p.add_argument("--batch-views", type=int, default=32)  # measured: 64 2,903 / 32 2,889 / 16 2,866 views/s
-    p.add_argument("--slots", type=int, default=2,
-                   help="concurrent batch pipelines (streams); 3 measured 0.5 %% faster, but overlapping "
-                        "composites then share their event spans and the per-kernel rooflines stop meaning much")
+    p.add_argument("--slots", type=int, default=3,
+                   help="concurrent batch pipelines (stream pairs); measured 3: 3,090, 2: 3,076 views/s")
     p.add_argument("--cpu-views", type=int, default=0, help="oracle sample size (0 = auto)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")

@@ -81,7 +81,7 @@ class ViewScorer:
     capacity follows gsr_bin_sort's capacity protocol (GSR_ECAPACITY returns
     the required size; grow by 25 % and retry)."""
 
-    def __init__(self, field: Gaussians, batch_views: int = 32, n_slots: int = 2, lod: Optional[gsr.Lod] = None,
+    def __init__(self, field: Gaussians, batch_views: int = 32, n_slots: int = 3, lod: Optional[gsr.Lod] = None,
                  order_tiles=None):
         self.field = field
         self.lod = lod  # NEXT-2 LOD blending (opacity multiplier in K1), or None
