@@ -1097,7 +1097,7 @@ constexpr int CS_AUTO_TPV = 4352;
 // view / chunk bookkeeping (K5 tail): vs[v] = first key of view v (vs[V] = K),
 // pb[v] = first chunk of view v (pb[V] = chunks)
 __device__ __forceinline__ void cs_locate(const uint32_t* __restrict__ meta, int V, uint32_t chunk, int& v,
-                                          uint32_t& k0, uint32_t& k1) {
+                                          uint32_t& k0, uint32_t& k1, uint32_t ch) {
   const uint32_t* vs = meta;
   const uint32_t* pb = meta + (V + 1);
   int lo = 0, hi = V - 1;
@@ -1106,12 +1106,12 @@ __device__ __forceinline__ void cs_locate(const uint32_t* __restrict__ meta, int
     if (pb[mid] <= chunk) lo = mid; else hi = mid - 1;
   }
   v = lo;
-  k0 = vs[v] + (chunk - pb[v]) * (uint32_t)CS_CHUNK;
-  k1 = min(k0 + (uint32_t)CS_CHUNK, vs[v + 1]);
+  k0 = vs[v] + (chunk - pb[v]) * ch;
+  k1 = min(k0 + ch, vs[v + 1]);
 }
 
 __global__ void __launch_bounds__(256) cs_meta(const uint2* __restrict__ ranges, int V, uint32_t tpv, uint32_t K,
-                                               uint32_t* __restrict__ meta) {
+                                               uint32_t* __restrict__ meta, uint32_t ch) {
   if (threadIdx.x != 0) return;
   uint32_t pb = 0;
   for (int v = 0; v <= V; ++v) {
@@ -1120,19 +1120,19 @@ __global__ void __launch_bounds__(256) cs_meta(const uint2* __restrict__ ranges,
     meta[(V + 1) + v] = pb;
     if (v < V) {
       const uint32_t e = (v + 1 < V) ? ranges[(size_t)(v + 1) * tpv].x : K;
-      pb += (e - s + CS_CHUNK - 1) / CS_CHUNK;
+      pb += (e - s + ch - 1) / ch;
     }
   }
 }
 
 __global__ void __launch_bounds__(256) cs_hist(const uint32_t* __restrict__ tkeys, const uint32_t* __restrict__ meta,
-                                               int V, uint32_t tpv, uint32_t* __restrict__ H, int gbits) {
+                                               int V, uint32_t tpv, uint32_t* __restrict__ H, int gbits, uint32_t ch) {
   extern __shared__ uint32_t s_h[];
   const uint32_t chunk = blockIdx.x;
   if (chunk >= meta[(V + 1) + V]) return;
   int v;
   uint32_t k0, k1;
-  cs_locate(meta, V, chunk, v, k0, k1);
+  cs_locate(meta, V, chunk, v, k0, k1, ch);
   for (uint32_t d = threadIdx.x; d < tpv; d += 256) s_h[d] = 0;
   __syncthreads();
   const uint32_t vb = (uint32_t)v * tpv;
@@ -1182,7 +1182,7 @@ __global__ void __launch_bounds__(W * 32, 3) cs_scatter(const uint32_t* __restri
                                                      const uint32_t* __restrict__ H,
                                                      uint32_t* __restrict__ vals_out, uint64_t* __restrict__ keys64,
                                                      const uint32_t* __restrict__ depth_plane, int64_t nper,
-                                                     int gbits) {
+                                                     int gbits, uint32_t ch) {
   // gbits > 0: packed words (tile within the view << gbits | g), no tvals
   // shared memory: s_base [tpv] u32 (chunk offset + keys so far), s_sub [tpv]
   // u32 (this sub-round's base), s_wh [W][tpv] u16 (per-warp counts, then
@@ -1203,7 +1203,7 @@ __global__ void __launch_bounds__(W * 32, 3) cs_scatter(const uint32_t* __restri
   if (chunk >= meta[(V + 1) + V]) return;
   int v;
   uint32_t k0, k1;
-  cs_locate(meta, V, chunk, v, k0, k1);
+  cs_locate(meta, V, chunk, v, k0, k1, ch);
   const uint32_t vb = (uint32_t)v * tpv + tb;
   const uint32_t* Hrow = H + (size_t)chunk * tpv + tb;
   for (uint32_t d = tid; d < tn; d += W * 32) s_base[d] = Hrow[d];
@@ -1262,29 +1262,27 @@ __global__ void __launch_bounds__(W * 32, 3) cs_scatter(const uint32_t* __restri
       }
     }
     __syncthreads();
-    // exclusive prefix over the warps, two tiles per 32-bit word (no carry:
-    // a sub-round holds at most W x 32 x CS_KPT < 2^16 keys)
-    const uint32_t* wh32 = reinterpret_cast<const uint32_t*>(s_wh);
-    for (uint32_t p = tid; p < ts / 2; p += W * 32) {
-      uint32_t run = 0;
+    // exclusive prefix over the warps, four tiles per 64-bit word (no carry:
+    // a sub-round holds at most W x 32 x CS_KPT < 2^16 keys); the bases of
+    // the word's four tiles move as one 16-byte vector (ts % 8 == 0; tiles
+    // >= tn are padding nobody reads)
+    uint64_t* wh64 = reinterpret_cast<uint64_t*>(s_wh);
+    for (uint32_t p = tid; p < ts / 4; p += W * 32) {
+      uint64_t run = 0;
 #pragma unroll
       for (int w = 0; w < W; ++w) {
-        uint32_t* q = const_cast<uint32_t*>(wh32) + (size_t)w * (ts / 2) + p;
-        const uint32_t c = *q;
+        uint64_t* q = wh64 + (size_t)w * (ts / 4) + p;
+        const uint64_t c = *q;
         *q = run;
         run += c;
       }
-      const uint32_t d = 2 * p;
-      if (d < tn) {
-        const uint32_t b = s_base[d];
-        s_sub[d] = b;
-        s_base[d] = b + (run & 0xffffu);
-      }
-      if (d + 1 < tn) {
-        const uint32_t b = s_base[d + 1];
-        s_sub[d + 1] = b;
-        s_base[d + 1] = b + (run >> 16);
-      }
+      uint4 b = reinterpret_cast<const uint4*>(s_base)[p];
+      reinterpret_cast<uint4*>(s_sub)[p] = b;
+      b.x += (uint32_t)run & 0xffffu;
+      b.y += (uint32_t)(run >> 16) & 0xffffu;
+      b.z += (uint32_t)(run >> 32) & 0xffffu;
+      b.w += (uint32_t)(run >> 48);
+      reinterpret_cast<uint4*>(s_base)[p] = b;
     }
     __syncthreads();
 #pragma unroll
@@ -1799,7 +1797,8 @@ static gsr_status bin_sort_impl(gsr_ctx* ctx, const uint32_t* bin_rec, int64_t n
   // GSR_TSORT=radix forces the two onesweep passes.
   if (use_cs) {
     // K4c counting scatter (default)
-    const uint64_t nchunks_max = (uint64_t)(K + CS_CHUNK - 1) / CS_CHUNK + (uint64_t)n_views;
+    const uint32_t ch = (uint32_t)CS_CHUNK;
+    const uint64_t nchunks_max = (uint64_t)(K + ch - 1) / ch + (uint64_t)n_views;
     void *hm, *meta;
     if ((s = ensure(ctx, S_CSH, nchunks_max * tpv * 4, &hm)) != GSR_OK) return s;
     if ((s = ensure(ctx, S_CSMETA, 2 * (n_views + 1) * 4, &meta)) != GSR_OK) return s;
@@ -1807,9 +1806,9 @@ static gsr_status bin_sort_impl(gsr_ctx* ctx, const uint32_t* bin_rec, int64_t n
     const uint32_t tslice = (uint32_t)((tpv + nslice - 1) / nslice);
     const size_t smem = (size_t)((tslice + 7) & ~7u) * (8 + 2 * 8);
     sp = stage_begin(ctx, GSR_STAGE_TILE_SORT, st);
-    cs_meta<<<1, 32, 0, st>>>((const uint2*)ranges, n_views, (uint32_t)tpv, (uint32_t)K, (uint32_t*)meta);
+    cs_meta<<<1, 32, 0, st>>>((const uint2*)ranges, n_views, (uint32_t)tpv, (uint32_t)K, (uint32_t*)meta, ch);
     cs_hist<<<(unsigned)nchunks_max, 256, tpv * 4, st>>>((const uint32_t*)tka, (const uint32_t*)meta, n_views,
-                                                          (uint32_t)tpv, (uint32_t*)hm, gbits);
+                                                          (uint32_t)tpv, (uint32_t*)hm, gbits, ch);
     cs_scan<<<(unsigned)((T + 255) / 256), 256, 0, st>>>((const uint2*)ranges, (const uint32_t*)meta, n_views,
                                                          (uint32_t)tpv, (uint32_t*)hm);
     const int dbits = std::max(1, bits_for(tslice));
@@ -1817,12 +1816,12 @@ static gsr_status bin_sort_impl(gsr_ctx* ctx, const uint32_t* bin_rec, int64_t n
     cudaFuncSetAttribute(scat, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     scat<<<(unsigned)(nchunks_max * nslice), 256, smem, st>>>(
         (const uint32_t*)tka, (const uint32_t*)tva, (const uint32_t*)meta, n_views, (uint32_t)tpv, dbits, tslice,
-        nslice, (const uint32_t*)hm, vals, keys, p_depth, n, gbits);
+        nslice, (const uint32_t*)hm, vals, keys, p_depth, n, gbits, ch);
     stage_end(ctx, sp, st);
     // hist reads 4 B/key; scatter reads 8 B/key (4 B packed) and writes the
     // 4-B values (+ 8-B keys when asked); the chunk x tile matrix is written,
     // scanned in place and read once
-    const double hbytes = (double)(K + CS_CHUNK - 1) / CS_CHUNK * (double)tpv * 4.0;
+    const double hbytes = (double)(K + ch - 1) / ch * (double)tpv * 4.0;
     account(ctx, GSR_STAGE_TILE_SORT, 4, ((gbits ? 12.0 : 16.0) + (keys ? 8.0 : 0.0)) * K + 4.0 * hbytes);
     if ((s = check_cuda(ctx, cudaGetLastError(), "tile counting scatter")) != GSR_OK) return s;
   } else {
