@@ -26,7 +26,9 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "gsr_oracle.c")
-_LIB = os.path.join(_HERE, "liboracle.so")
+# GSR_ORACLE_LIB: a prebuilt (e.g. deliberately mutated) oracle library, for
+# scripts/oracle_mutants.py only; build() never overwrites it
+_LIB = os.environ.get("GSR_ORACLE_LIB") or os.path.join(_HERE, "liboracle.so")
 
 CFLAGS = ["-O2", "-std=c11", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared"]
 
@@ -57,6 +59,8 @@ def _lod(lod):
 
 def build(force: bool = False) -> str:
     """Compile the oracle with gcc (no fast-math, no FMA contraction)."""
+    if os.environ.get("GSR_ORACLE_LIB"):
+        return _LIB
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
         cmd = ["gcc", *CFLAGS, "-o", _LIB, _SRC, "-lm", "-lpthread"]
         subprocess.check_call(cmd)

@@ -101,12 +101,14 @@ gsr_status gsr_create(gsr_ctx** out, int device) {
 
 gsr_status gsr_timing_enable(gsr_ctx* ctx, int enable) {
   if (!ctx) return GSR_EINVAL;
+  DeviceGuard device_guard(ctx);
   ctx->timing = enable != 0;
   return GSR_OK;
 }
 
 gsr_status gsr_timing_read(gsr_ctx* ctx, double* ms, int64_t* launches, double* bytes) {
   if (!ctx) return GSR_EINVAL;
+  DeviceGuard device_guard(ctx);
   double acc[GSR_N_STAGES] = {};
   for (auto& s : ctx->spans) {
     cudaError_t e = cudaEventSynchronize(s.b);
@@ -130,6 +132,7 @@ gsr_status gsr_timing_read(gsr_ctx* ctx, double* ms, int64_t* launches, double* 
 
 gsr_status gsr_destroy(gsr_ctx* ctx) {
   if (!ctx) return GSR_EINVAL;
+  DeviceGuard device_guard(ctx);
   cudaSetDevice(ctx->device);
   for (auto& s : ctx->spans) {
     cudaEventDestroy(s.a);
@@ -198,6 +201,7 @@ gsr_status gsr_camera_look_at(double elevation, double azimuth, double radius, c
 gsr_status gsr_project(gsr_ctx* ctx, const gsr_gaussians* G, const gsr_camera* cams, int32_t n_views,
                        const gsr_lod* lod, float* render_rec, uint32_t* bin_rec, void* stream) {
   if (!ctx) return GSR_EINVAL;
+  DeviceGuard device_guard(ctx);
   if (!G || !cams || !render_rec || !bin_rec) return set_err(ctx, GSR_EINVAL, "gsr_project: NULL required pointer");
   if (G->n < 0 || G->sh_degree < 0 || G->sh_degree > 3)
     return set_err(ctx, GSR_EINVAL, "gsr_project: n < 0 or sh_degree not in [0,3]");

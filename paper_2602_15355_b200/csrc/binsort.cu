@@ -1546,6 +1546,7 @@ extern "C" gsr_status gsr_sort_pairs_u64(gsr_ctx* ctx, const uint64_t* keys_in, 
                                          uint64_t* keys_out, uint32_t* vals_out, int64_t n, int32_t begin_bit,
                                          int32_t end_bit, void* stream) {
   if (!ctx) return GSR_EINVAL;
+  DeviceGuard device_guard(ctx);
   if (n < 0 || n >= (1ll << 31)) return set_err(ctx, GSR_EINVAL, "gsr_sort_pairs_u64: n out of range");
   if (begin_bit < 0 || end_bit > 64 || begin_bit >= end_bit)
     return set_err(ctx, GSR_EINVAL, "gsr_sort_pairs_u64: bad bit range");
@@ -1589,6 +1590,7 @@ static gsr_status bin_sort_impl(gsr_ctx* ctx, const uint32_t* bin_rec, int64_t n
                                 uint32_t* ranges, uint64_t* keys_unsorted, uint32_t* vals_unsorted,
                                 const CachedOrder* co, void* stream) {
   if (!ctx) return GSR_EINVAL;
+  DeviceGuard device_guard(ctx);
   if (!bin_rec || !cams || !vals || !n_keys || !ranges)
     return set_err(ctx, GSR_EINVAL, "gsr_bin_sort: NULL required pointer");
   if (n < 0 || n_views <= 0 || n_views > GSR_MAX_VIEWS || capacity < 0)
@@ -1897,6 +1899,7 @@ extern "C" int64_t gsr_order_cache_size(const int64_t* tile_start, int32_t n_til
 extern "C" gsr_status gsr_build_order_cache(gsr_ctx* ctx, const gsr_gaussians* G, const int64_t* tile_start,
                                             int32_t n_tiles, const int32_t* bins, uint32_t* cache, void* stream) {
   if (!ctx) return GSR_EINVAL;
+  DeviceGuard device_guard(ctx);
   if (!G || !cache) return set_err(ctx, GSR_EINVAL, "gsr_build_order_cache: NULL required pointer");
   gsr_status s;
   if ((s = check_tiles(ctx, tile_start, n_tiles, bins, G->n, "gsr_build_order_cache")) != GSR_OK) return s;
@@ -1943,6 +1946,7 @@ extern "C" gsr_status gsr_bin_sort_cached(gsr_ctx* ctx, const uint32_t* bin_rec,
                                           uint64_t* keys, uint32_t* vals, int64_t capacity, int64_t* n_keys,
                                           uint32_t* ranges, void* stream) {
   if (!ctx) return GSR_EINVAL;
+  DeviceGuard device_guard(ctx);
   if (!cache || !centres || !cams) return set_err(ctx, GSR_EINVAL, "gsr_bin_sort_cached: NULL required pointer");
   if (n_views <= 0 || n_views > GSR_MAX_VIEWS) return set_err(ctx, GSR_EINVAL, "gsr_bin_sort_cached: bad n_views");
   gsr_status s;

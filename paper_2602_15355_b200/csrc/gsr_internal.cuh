@@ -161,6 +161,24 @@ struct gsr_ctx {
 
 namespace gsr {
 
+// Every entry point runs on the context's device: libgsr links cudart
+// statically, so it keeps its own per-thread current device, which another
+// thread or a second context may have left elsewhere.  The caller's device
+// is restored on return.
+struct DeviceGuard {
+  int prev = -1;
+  bool restore = false;
+  explicit DeviceGuard(const gsr_ctx* ctx) {
+    if (ctx && cudaGetDevice(&prev) == cudaSuccess && prev != ctx->device)
+      restore = cudaSetDevice(ctx->device) == cudaSuccess;
+  }
+  ~DeviceGuard() {
+    if (restore) cudaSetDevice(prev);
+  }
+  DeviceGuard(const DeviceGuard&) = delete;
+  DeviceGuard& operator=(const DeviceGuard&) = delete;
+};
+
 gsr_status set_err(gsr_ctx* ctx, gsr_status st, const std::string& msg);
 gsr_status check_cuda(gsr_ctx* ctx, cudaError_t e, const char* what);
 gsr_status ensure(gsr_ctx* ctx, Slot s, size_t bytes, void** out);

@@ -94,6 +94,7 @@ using namespace gsr;
 extern "C" gsr_status gsr_l2_loss(gsr_ctx* ctx, const float* img, const float* target, int64_t n_pixels,
                                   const float* weights, float* dl_dimg, double* loss, void* stream) {
   if (!ctx) return GSR_EINVAL;
+  DeviceGuard device_guard(ctx);
   if (!img || !target || !weights || !loss) return set_err(ctx, GSR_EINVAL, "gsr_l2_loss: NULL required pointer");
   if (n_pixels <= 0) return set_err(ctx, GSR_EINVAL, "gsr_l2_loss: n_pixels <= 0");
   cudaStream_t st = (cudaStream_t)stream;
@@ -114,6 +115,7 @@ extern "C" gsr_status gsr_adam_step(gsr_ctx* ctx, float* params, const float* gr
                                     int32_t planes, const float* lr, float beta1, float beta2, float eps,
                                     int32_t step, void* stream) {
   if (!ctx) return GSR_EINVAL;
+  DeviceGuard device_guard(ctx);
   if (!params || !grads || !m || !v || !lr) return set_err(ctx, GSR_EINVAL, "gsr_adam_step: NULL required pointer");
   if (n < 0 || planes < 2 || planes > 16 || step < 1 || !(beta1 >= 0.0f && beta1 < 1.0f) ||
       !(beta2 >= 0.0f && beta2 < 1.0f) || !(eps > 0.0f))

@@ -51,6 +51,7 @@ using namespace gsr;
 extern "C" gsr_status gsr_select_nbv(gsr_ctx* ctx, const float* scores, int32_t n, const uint8_t* exclude, int32_t k,
                                      int32_t* out_idx, void* stream) {
   if (!ctx) return GSR_EINVAL;
+  DeviceGuard device_guard(ctx);
   if (!scores || !out_idx) return set_err(ctx, GSR_EINVAL, "gsr_select_nbv: NULL required pointer");
   if (n <= 0 || n > 16384) return set_err(ctx, GSR_EINVAL, "gsr_select_nbv: n must be in [1, 16384]");
   int excluded = 0;

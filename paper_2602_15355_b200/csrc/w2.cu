@@ -125,6 +125,7 @@ using namespace gsr;
 extern "C" gsr_status gsr_w2_scores(gsr_ctx* ctx, const float* mu, const float* s2, int32_t n_views, int32_t M,
                                     int32_t C, int64_t HW, float* scores, float* map, void* stream) {
   if (!ctx) return GSR_EINVAL;
+  DeviceGuard device_guard(ctx);
   if (!mu || !s2 || !scores) return set_err(ctx, GSR_EINVAL, "gsr_w2_scores: NULL required pointer");
   if (n_views <= 0 || M < 2 || C < 1 || HW < 1)
     return set_err(ctx, GSR_EINVAL, "gsr_w2_scores: need n_views >= 1, M >= 2, C >= 1, HW >= 1");

@@ -12,6 +12,7 @@ import os
 from typing import Optional
 
 import numpy as np
+import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("GSR_LIB") or os.path.join(_HERE, "libgsr.so")
@@ -139,9 +140,17 @@ class Gaussians:
     """Device-resident packed field: planes[P][n][4] float32 CUDA tensor."""
 
     def __init__(self, planes, sh_degree: int):
-        assert planes.is_cuda and planes.dtype.is_floating_point and planes.shape[-1] == 4
+        # the kernels read float4 planes: any other dtype would be misread silently
+        if not planes.is_cuda or planes.dtype != torch.float32 or planes.dim() != 3 or planes.shape[-1] != 4:
+            raise ValueError("Gaussians: planes must be a CUDA float32 tensor [P][n][4]")
+        sh_degree = int(sh_degree)
+        if not 0 <= sh_degree <= 3:
+            raise ValueError("Gaussians: sh_degree must be in [0, 3]")
+        need = 3 + (3 * (sh_degree + 1) ** 2 + 3) // 4  # (x,y,z,o), (s,u), q, SH slots
+        if planes.shape[0] < need:
+            raise ValueError(f"Gaussians: {planes.shape[0]} planes, degree {sh_degree} needs {need}")
         self.planes = planes.contiguous()
-        self.sh_degree = int(sh_degree)
+        self.sh_degree = sh_degree
         self.n = int(planes.shape[1])
 
     def struct(self) -> _Gaussians:
@@ -155,7 +164,8 @@ class Lod:
     (tile centre x, y, z, level) + levels, bandwidth delta and thresholds."""
 
     def __init__(self, tile_level, levels: int, delta: float, thresholds):
-        assert tile_level.is_cuda and tile_level.dtype.is_floating_point and tile_level.shape[-1] == 4
+        if not tile_level.is_cuda or tile_level.dtype != torch.float32 or tile_level.shape[-1] != 4:
+            raise ValueError("Lod: tile_level must be a CUDA float32 tensor [n][4]")
         self.tile_level = tile_level.contiguous()
         self.levels = int(levels)
         self.delta = float(delta)

@@ -42,7 +42,15 @@ def _worker(rank, world, port, out_q, mode):
     try:
         sc = synth.make_scene(1, n_override=1500, views=10)
         cams = synth.with_resolution(sc.cameras, 48, 48, 48.0)
-        if mode == "flat":
+        if mode == "bcast":
+            # C1: rank 0 holds the packed field, the others start from zeros
+            planes = torch.from_numpy(sc.field.planes.copy()) if rank == 0 else torch.zeros(sc.field.planes.shape)
+            D.broadcast_field(planes)
+            fld = synth.GaussianField(planes.numpy(), sc.field.sh_degree)
+            scores, sel = D.score_and_select(cams, _oracle_scorer(fld), _select, k=3)
+            out_q.put((rank, planes.numpy().tobytes() == sc.field.planes.tobytes(), scores.numpy().tolist(),
+                       sel.numpy().tolist()))
+        elif mode == "flat":
             scores, sel = D.score_and_select(cams, _oracle_scorer(sc.field), _select, k=3)
             out_q.put((rank, scores.numpy().tolist(), sel.numpy().tolist()))
         else:
@@ -94,6 +102,19 @@ def test_gloo_score_gather_select(world):
     res = _run(world, "flat")
     exp_sel = oracle.select_topk(np.float32(ref), 3).tolist()
     for rank, scores, sel in res:
+        assert np.array_equal(np.float32(scores), np.float32(ref)), rank
+        assert sel == exp_sel
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_gloo_broadcast_field_then_score(world):
+    """C1: after broadcast_field every rank holds rank 0's field bytes, and
+    scoring from the broadcast copies reproduces the single-process scores."""
+    sc, cams, ref = _reference()
+    res = _run(world, "bcast")
+    exp_sel = oracle.select_topk(np.float32(ref), 3).tolist()
+    for rank, same, scores, sel in res:
+        assert same, rank
         assert np.array_equal(np.float32(scores), np.float32(ref)), rank
         assert sel == exp_sel
 
