@@ -213,11 +213,14 @@ __global__ void __launch_bounds__(256) k1_project(const float4* __restrict__ po,
           const float len = sqrtf((dx * dx + dy * dy) + dz * dz);
           float rgb[3];
           sh_colour<DEG>(S, dx / len, dy / len, dz / len, rgb);
-          // conservative half-extents of {q <= thr}: sqrt(thr * Sigma'_xx), rounded up to fp16
+          // conservative half-extents of {q <= thr}: sqrt(thr * Sigma'_xx), rounded up to fp16;
+          // beyond the fp16 range (65,504 px) the round-up gives +inf, so K6's box test
+          // always passes (a clamp to 65,504 culled huge Gaussians whose mean lies far
+          // off-screen: tests/test_gpu_adversarial.py "huge_offscreen")
           float ex = 0.0f, ey = 0.0f;
           if (thr > 0.0f) {
-            ex = fminf(sqrtf(thr * a) * 1.001f + 0.05f, 65504.0f);
-            ey = fminf(sqrtf(thr * cc) * 1.001f + 0.05f, 65504.0f);
+            ex = sqrtf(thr * a) * 1.001f + 0.05f;
+            ey = sqrtf(thr * cc) * 1.001f + 0.05f;
           }
           const uint32_t ext = (uint32_t)__half_as_ushort(__float2half_ru(ex)) |
                                ((uint32_t)__half_as_ushort(__float2half_ru(ey)) << 16);

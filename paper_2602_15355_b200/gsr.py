@@ -147,7 +147,7 @@ class Gaussians:
         if not 0 <= sh_degree <= 3:
             raise ValueError("Gaussians: sh_degree must be in [0, 3]")
         need = 3 + (3 * (sh_degree + 1) ** 2 + 3) // 4  # (x,y,z,o), (s,u), q, SH slots
-        if planes.shape[0] < need:
+        if planes.shape[1] > 0 and planes.shape[0] < need:  # an empty field reads no plane
             raise ValueError(f"Gaussians: {planes.shape[0]} planes, degree {sh_degree} needs {need}")
         self.planes = planes.contiguous()
         self.sh_degree = sh_degree
