@@ -34,17 +34,17 @@ def deps():
         os.path.join(HERE, "..", "include", "gsr.h"), __file__]
 
 
-def needs_build() -> bool:
-    if not os.path.exists(LIB):
+def needs_build(lib: str = LIB) -> bool:
+    if not os.path.exists(lib):
         return True
-    t = os.path.getmtime(LIB)
+    t = os.path.getmtime(lib)
     return any(os.path.getmtime(d) > t for d in deps())
 
 
 def build(force: bool = False, verbose: bool = False, debug: bool = False) -> str:
     lib = LIB.replace("libgsr.so", "libgsr_debug.so") if debug else LIB
-    if not force and not debug and not needs_build():
-        return LIB
+    if not force and not needs_build(lib):
+        return lib
     tmp = lib + ".tmp"
     extra = ["-DGSR_DEBUG"] if debug else []
     cmd = [NVCC, *NVCC_FLAGS, *extra, "-shared", "-o", tmp, *sources(),

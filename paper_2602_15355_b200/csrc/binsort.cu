@@ -230,6 +230,7 @@ __global__ void __launch_bounds__(256, K2_MINB) k2_compact(const uint32_t* __res
   const uint64_t pv0 = s_pv;
   for (uint32_t j = tid; j < bt; j += 256) {
     const KeyT key = s_key[j];
+    GSR_DCHECK(pv0 + j < (uint64_t)M);
     dkeys[pv0 + j] = key;
     dvals[pv0 + j] = s_g[j];
     for (int p = 0; p < dpasses; ++p) atomicAdd(&s_hist[p][(uint32_t)(key >> (8 * p)) & 255], 1u);
@@ -825,7 +826,7 @@ __global__ void __launch_bounds__(256, K3_MINB) k3_emit(const KeyT* __restrict__
                                                uint32_t tpv, int W, uint32_t* __restrict__ tkeys,
                                                uint32_t* __restrict__ tvals, uint32_t* __restrict__ counts,
                                                uint64_t* __restrict__ lb, uint32_t* __restrict__ ctr,
-                                               int smem_bins, int vshift, int gbits) {
+                                               int smem_bins, int vshift, int gbits, uint64_t kcap, uint64_t T) {
   // gbits > 0: each key leaves as ONE packed word (tile within its view <<
   // gbits | g) in tkeys and tvals is not written (the K4c path unpacks it)
   // Per-tile counts: a shared-memory histogram over the tiles of the block's
@@ -862,6 +863,7 @@ __global__ void __launch_bounds__(256, K3_MINB) k3_emit(const KeyT* __restrict__
       const KeyT key = dkeys[e];
       g[r] = dvals[e];
       view[r] = (uint32_t)(key >> vshift);
+      GSR_DCHECK(g[r] < n);
       const int64_t pi = (int64_t)view[r] * n + g[r];
       s0[r] = __ldg(span + 2 * pi);
       s1[r] = __ldg(span + 2 * pi + 1);
@@ -929,6 +931,7 @@ __global__ void __launch_bounds__(256, K3_MINB) k3_emit(const KeyT* __restrict__
         const uint32_t okl = __shfl_sync(FULL, kl, t);
         if (k < wt) {
           const uint32_t key = okb + (k - owx);
+          GSR_DCHECK(base + k < kcap && key < T);
           if (PACK) {
             tkeys[base + k] = okl + ((k - owx) << gbits);
           } else {
@@ -1137,7 +1140,10 @@ __global__ void __launch_bounds__(256) cs_hist(const uint32_t* __restrict__ tkey
   __syncthreads();
   const uint32_t vb = (uint32_t)v * tpv;
   if (gbits)
-    for (uint32_t i = k0 + threadIdx.x; i < k1; i += 256) atomicAdd(s_h + (__ldg(tkeys + i) >> gbits), 1u);
+    for (uint32_t i = k0 + threadIdx.x; i < k1; i += 256) {
+      GSR_DCHECK((__ldg(tkeys + i) >> gbits) < tpv);
+      atomicAdd(s_h + (__ldg(tkeys + i) >> gbits), 1u);
+    }
   else
     for (uint32_t i = k0 + threadIdx.x; i < k1; i += 256) atomicAdd(s_h + (__ldg(tkeys + i) - vb), 1u);
   __syncthreads();
@@ -1289,6 +1295,7 @@ __global__ void __launch_bounds__(W * 32, 3) cs_scatter(const uint32_t* __restri
     for (int k = 0; k < CS_KPT; ++k) {
       if (dg[k] < tn) {
         const uint32_t pos = s_sub[dg[k]] + (uint32_t)wh[dg[k]] + rk[k];
+        GSR_DCHECK(pos >= meta[v] && pos < meta[v + 1]);  // inside its view's key range
         vals_out[pos] = vv[k];
         if (keys64) keys64[pos] = ((uint64_t)(vb + dg[k]) << 32) | __ldg(depth_plane + (int64_t)v * nper + vv[k]);
       }
@@ -1767,13 +1774,13 @@ static gsr_status bin_sort_impl(gsr_ctx* ctx, const uint32_t* bin_rec, int64_t n
     cudaFuncSetAttribute(k3, cudaFuncAttributeMaxDynamicSharedMemorySize, bins * 4);
     k3<<<(unsigned)nb3, 256, bins * 4, st>>>((const uint64_t*)ck, cvv, nvis, p_span, n, gx, (uint32_t)tpv, W,
                                              (uint32_t*)tka, (uint32_t*)tva, (uint32_t*)cnt, lb3, ctrs + 5, bins,
-                                             32, gbits);
+                                             32, gbits, (uint64_t)K, T);
   } else {
     auto k3 = gbits ? k3_emit<uint32_t, true> : k3_emit<uint32_t, false>;
     cudaFuncSetAttribute(k3, cudaFuncAttributeMaxDynamicSharedMemorySize, bins * 4);
     k3<<<(unsigned)nb3, 256, bins * 4, st>>>((const uint32_t*)ck, cvv, nvis, p_span, n, gx, (uint32_t)tpv, W,
                                              (uint32_t*)tka, (uint32_t*)tva, (uint32_t*)cnt, lb3, ctrs + 5, bins,
-                                             co ? cshift : dshift, gbits);
+                                             co ? cshift : dshift, gbits, (uint64_t)K, T);
   }
   stage_end(ctx, sp, st);
   account(ctx, GSR_STAGE_EMIT, 1, 44.0 * nvis + (gbits ? 4.0 : 8.0) * K + 4.0 * T);

@@ -15,6 +15,24 @@
 
 #include "../../include/gsr.h"
 
+// Device-side bounds checks of the debug build (build.py --debug ->
+// libgsr_debug.so, GSR_LIB=...): compute-sanitizer is closed on the GPU
+// pool, so every computed global index of the hot kernels is checked here
+// and a violation traps with its location.
+#ifdef GSR_DEBUG
+#define GSR_DCHECK(cond)                                                          \
+  do {                                                                            \
+    if (!(cond)) {                                                                \
+      printf("GSR_DCHECK failed %s:%d: %s\n", __FILE__, __LINE__, #cond);         \
+      __trap();                                                                   \
+    }                                                                             \
+  } while (0)
+#else
+#define GSR_DCHECK(cond) \
+  do {                   \
+  } while (0)
+#endif
+
 namespace gsr {
 
 // ---- rasterizer constants (float32 hex in comments) ----
