@@ -111,6 +111,19 @@ class ClockSampler:
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(rows)}
 
 
+def cpu_model() -> str:
+    """The host CPU's model name (/proc/cpuinfo), for the CPU baselines."""
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
 # ----------------------------------------------------------------------------- reference arm
 def run_reference(args, scene, cfg_json):
     import oracle
@@ -141,7 +154,8 @@ def run_reference(args, scene, cfg_json):
             "steps": len(times), "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": cfg_json,
             "fragments_per_sec": fr / t,
-            "cpu_baseline": {"value": v, "unit": UNIT, "cores": n_threads, "kind": "oracle", "sample": sample},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": n_threads, "cpu_model": cpu_model(), "kind": "oracle",
+                             "sample": sample},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
 
@@ -155,7 +169,7 @@ def cpu_baseline(scene, n_views: int):
     t0 = time.perf_counter()
     scores, nf, nk, _ = oracle.render_views(scene.field, cams, n_threads=n_threads)
     dt = time.perf_counter() - t0
-    return {"value": nv / dt, "unit": UNIT, "cores": n_threads, "kind": "oracle",
+    return {"value": nv / dt, "unit": UNIT, "cores": n_threads, "cpu_model": cpu_model(), "kind": "oracle",
             "sample": f"{nv} strided views of the 1,024 at 800x800 (1M Gaussians), full O1-O6 oracle, "
                       f"{dt:.1f} s wall on {n_threads} threads", "fragments_per_sec": float(nf.sum()) / dt}
 
@@ -546,7 +560,7 @@ def main():
 
     # the same K6 roofline with K6 alone on the GPU (one slot, one step): the
     # two-stream spans above include time the composite shares with the sorts
-    iso = iso_sort = None
+    iso = iso_sort = iso_stages = with_maps = None
     if not args.no_extras and world == 1:
         iso_scorer = ViewScorer(G, batch_views=args.batch_views, n_slots=1)
         iso_scorer.score_views(cams)
@@ -570,8 +584,37 @@ def main():
                     "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": round(iso_sort_gbs / peaks["hbm_gbs"], 4),
                     "ms_per_step": round(ist["tile_sort"]["ms"], 2),
                     "share_of_serial_step": round(ist["tile_sort"]["ms"] / sum(v["ms"] for v in ist.values()), 3)}
+        # every stage alone on one stream (the kernels' own rates; inside the
+        # pipeline a stage's event spans also hold time it waits for SMs)
+        iso_stages = {k: {"ms_per_step": round(v["ms"], 3),
+                          "algo_GB_per_step": round(v["bytes"] / 1e9, 3),
+                          "GB_per_s": round(v["bytes"] / (v["ms"] / 1e3) / 1e9, 1) if v["ms"] > 0 else None,
+                          "frac_hbm": round(v["bytes"] / (v["ms"] / 1e3) / 1e9 / peaks["hbm_gbs"], 4)
+                          if v["ms"] > 0 else None}
+                      for k, v in ist.items() if v["launches"]}
         iso_scorer.timing(False)
         del iso_scorer
+        torch.cuda.empty_cache()
+        # the same step also writing every view's (r, g, b, U) map (north_star:
+        # "with oracle-matching maps"): 1,024 x 800 x 800 x 16 B = 10.5 GB
+        # written per step into one resident tensor
+        maps = torch.empty((1024, 800, 800, 4), dtype=torch.float32, device=dev)
+        sc_m = torch.empty(1024, dtype=torch.float32, device=dev)
+        scorer.score_views(cams, sc_m, images_out=maps)
+        barrier()
+        em0, em1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        em0.record()
+        for _ in range(args.steps):
+            scorer.score_views(cams, sc_m, images_out=maps)
+            scorer.select(sc_m, 1)
+        em1.record()
+        barrier()
+        mms = em0.elapsed_time(em1) / args.steps
+        with_maps = {"value": round(1024 / (mms / 1e3), 2), "unit": UNIT, "ms_per_step": round(mms, 3),
+                     "maps_GB_per_step": round(maps.numel() * 4 / 1e9, 2),
+                     "what": "the timed step with every view's RGBU map written to a resident [1024][800][800][4] "
+                             "float tensor"}
+        del maps
         torch.cuda.empty_cache()
 
     # the two collectives timed on their own (CUDA events on
@@ -611,7 +654,7 @@ def main():
             # for SMs the composite holds (kept as roofline_sort_pipeline)
             "roofline_sort": iso_sort if iso_sort is not None else roof_sort,
             "roofline_sort_pipeline": roof_sort,
-            "stages": stage_tab,
+            "stages": stage_tab, "stages_single_stream": iso_stages, "with_maps": with_maps,
             "gpu_launches": int(launches * world), "clocks": clk, "e2e": e2e, "collectives": coll,
             "keys_per_step_rank0": int(sum(scorer.last_keys))}
     if rank == 0 and world == 1 and not args.no_extras:  # single-GPU extras (skipped in the scaling runs)

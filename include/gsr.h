@@ -195,6 +195,17 @@ gsr_status gsr_bin_sort(gsr_ctx* ctx, const uint32_t* bin_rec, int64_t n, const 
      the lower tile); the visible Gaussians are emitted in that order, so every
      tile list is composited in it (approximate: not the exact depth order).
      Same outputs and errors as gsr_bin_sort (keys: low word = depth bits). */
+/* gsr_order_cache_bins: the cache policy of PAPER.md §3.5 L121-122 ("tiles
+     whose uncertainty exceeds threshold tau retain a larger set of cached
+     orderings"; tau = 0.6, §3.6): bins[t] = hot_bins if the mean
+     per-Gaussian uncertainty of tile t (Gaussians [tile_start[t],
+     tile_start[t+1]), double sum) exceeds tau, else base_bins.  tile_start
+     [host] int64 [n_tiles + 1] covering [0, n); bins [host] int32 [n_tiles].
+     SYNC (one n_tiles x 4-byte readback).  EINVAL: NULL pointers, n_tiles not
+     in [1, 4096], bins not in [1, 64], ranges not covering [0, n). */
+gsr_status gsr_order_cache_bins(gsr_ctx* ctx, const gsr_gaussians* gaussians, const int64_t* tile_start,
+                                int32_t n_tiles, float tau, int32_t base_bins, int32_t hot_bins, int32_t* bins,
+                                void* stream);
 int64_t gsr_order_cache_size(const int64_t* tile_start, int32_t n_tiles, const int32_t* bins);
 gsr_status gsr_build_order_cache(gsr_ctx* ctx, const gsr_gaussians* gaussians, const int64_t* tile_start,
                                  int32_t n_tiles, const int32_t* bins, uint32_t* cache, void* stream);

@@ -32,6 +32,12 @@ TAU = 0.6
 BASE_BINS, HOT_BINS = 8, 16
 
 
+def tile_mean_uncertainty(field, tile_start) -> np.ndarray:
+    """Mean per-Gaussian uncertainty of each tile (the cache policy input)."""
+    u = field.planes[1, :, 3].astype(np.float64)
+    return np.array([u[tile_start[t]:tile_start[t + 1]].mean() for t in range(len(tile_start) - 1)])
+
+
 def bins_for(u_bar, tau: float = TAU):
     """Cache policy: hot tiles (mean uncertainty > tau) keep 16 bins, else 8."""
     return HOT_BINS if float(u_bar) > tau else BASE_BINS

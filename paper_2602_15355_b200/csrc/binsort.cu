@@ -1947,6 +1947,30 @@ extern "C" gsr_status gsr_build_order_cache(gsr_ctx* ctx, const gsr_gaussians* G
   return gsr_sort_pairs_u64(ctx, keys, vals, keys_out, cache, N, 0, end_bit, stream);
 }
 
+// NEXT-2b cache policy (§3.5 "tiles whose uncertainty
+// exceeds threshold tau retain a larger set of cached orderings", tau = 0.6
+// §3.6): per tile the mean per-Gaussian uncertainty (double, fixed-order
+// block sum), hot_bins if it exceeds tau, else base_bins.
+__global__ void __launch_bounds__(256) k_cache_bins(const float4* __restrict__ su, const int64_t* __restrict__ start,
+                                                    float tau, int32_t base_bins, int32_t hot_bins,
+                                                    int32_t* __restrict__ bins) {
+  __shared__ double s_w[8];
+  const int t = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t a = start[t], b = start[t + 1];
+  double acc = 0.0;
+  for (int64_t i = a + tid; i < b; i += 256) acc += (double)__ldg(&su[i].w);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(FULL, acc, o);
+  if (lane == 0) s_w[warp] = acc;
+  __syncthreads();
+  if (tid == 0) {
+    double sum = 0.0;
+    for (int w = 0; w < 8; ++w) sum += s_w[w];
+    const double mean = b > a ? sum / (double)(b - a) : 0.0;
+    bins[t] = mean > (double)tau ? hot_bins : base_bins;
+  }
+}
+
 extern "C" gsr_status gsr_bin_sort_cached(gsr_ctx* ctx, const uint32_t* bin_rec, int64_t n, const gsr_camera* cams,
                                           int32_t n_views, const uint32_t* cache, const int64_t* tile_start,
                                           int32_t n_tiles, const int32_t* bins, const double* centres,
@@ -2010,4 +2034,36 @@ extern "C" gsr_status gsr_bin_sort_cached(gsr_ctx* ctx, const uint32_t* bin_rec,
   CachedOrder co{(const OrderSeg*)tab, n_tiles, cache};
   return bin_sort_impl(ctx, bin_rec, n, cams, n_views, keys, vals, capacity, n_keys, ranges, nullptr, nullptr, &co,
                        stream);
+}
+
+extern "C" gsr_status gsr_order_cache_bins(gsr_ctx* ctx, const gsr_gaussians* G, const int64_t* tile_start,
+                                           int32_t n_tiles, float tau, int32_t base_bins, int32_t hot_bins,
+                                           int32_t* bins, void* stream) {
+  if (!ctx) return GSR_EINVAL;
+  DeviceGuard device_guard(ctx);
+  if (!G || !tile_start || !bins || n_tiles <= 0 || n_tiles > 4096)
+    return set_err(ctx, GSR_EINVAL, "gsr_order_cache_bins: NULL pointer or bad n_tiles");
+  if (base_bins < 1 || base_bins > 64 || hot_bins < 1 || hot_bins > 64)
+    return set_err(ctx, GSR_EINVAL, "gsr_order_cache_bins: bins in [1, 64]");
+  if (tile_start[0] != 0 || tile_start[n_tiles] != G->n)
+    return set_err(ctx, GSR_EINVAL, "gsr_order_cache_bins: tile ranges must cover [0, n)");
+  for (int t = 0; t < n_tiles; ++t)
+    if (tile_start[t + 1] < tile_start[t]) return set_err(ctx, GSR_EINVAL, "gsr_order_cache_bins: tile ranges");
+  cudaStream_t st = (cudaStream_t)stream;
+  gsr_status s;
+  void* tab;
+  const size_t tb = (size_t)(n_tiles + 1) * 8 + (size_t)n_tiles * 4;
+  if ((s = ensure(ctx, S_SELECT2, tb, &tab)) != GSR_OK) return s;
+  int64_t* d_start = (int64_t*)tab;
+  int32_t* d_bins = (int32_t*)((char*)tab + (size_t)(n_tiles + 1) * 8);
+  if ((s = check_cuda(ctx, cudaMemcpyAsync(d_start, tile_start, (size_t)(n_tiles + 1) * 8, cudaMemcpyHostToDevice, st),
+                      "tile table")) != GSR_OK)
+    return s;
+  k_cache_bins<<<n_tiles, 256, 0, st>>>(reinterpret_cast<const float4*>(G->scale_unc), d_start, tau, base_bins,
+                                         hot_bins, d_bins);
+  if ((s = check_cuda(ctx, cudaGetLastError(), "k_cache_bins")) != GSR_OK) return s;
+  if ((s = check_cuda(ctx, cudaMemcpyAsync(bins, d_bins, (size_t)n_tiles * 4, cudaMemcpyDeviceToHost, st), "bins")) !=
+      GSR_OK)
+    return s;
+  return check_cuda(ctx, cudaStreamSynchronize(st), "gsr_order_cache_bins sync");
 }

@@ -34,7 +34,7 @@ EXPORTED = ["gsr_create", "gsr_destroy", "gsr_last_error", "gsr_version", "gsr_c
             "gsr_project", "gsr_bin_sort", "gsr_composite", "gsr_score_views", "gsr_select_nbv",
             "gsr_sort_pairs_u64", "gsr_scratch_bytes", "gsr_timing_enable", "gsr_timing_read", "gsr_w2_scores",
             "gsr_sobel_scores", "gsr_backward", "gsr_order_cache_size", "gsr_build_order_cache",
-            "gsr_bin_sort_cached", "gsr_l2_loss", "gsr_adam_step"]
+            "gsr_bin_sort_cached", "gsr_l2_loss", "gsr_adam_step", "gsr_order_cache_bins"]
 STAGES = ["project", "compact", "depth_sort", "emit", "ranges", "tile_sort", "composite", "score", "select",
           "sort_u64", "w2", "sobel", "backward", "optim"]
 
@@ -75,6 +75,7 @@ def _load():
     L.gsr_backward.argtypes = [P, P, P, i32, P, P, P, P, P, P, P, P, P]
     L.gsr_l2_loss.argtypes = [P, P, P, i64, P, P, P, P]
     L.gsr_adam_step.argtypes = [P, P, P, P, P, i64, i32, P, ctypes.c_float, ctypes.c_float, ctypes.c_float, i32, P]
+    L.gsr_order_cache_bins.argtypes = [P, P, P, i32, ctypes.c_float, i32, i32, P, P]
     L.gsr_order_cache_size.argtypes = [P, i32, P]
     L.gsr_order_cache_size.restype = i64
     L.gsr_build_order_cache.argtypes = [P, P, P, i32, P, P, P]
@@ -275,6 +276,18 @@ def gsr_bin_sort_cached(ctx: Context, bin_rec, n: int, cams, oc: OrderCache, val
         raise e
     ctx._check(st)
     return int(nk.value)
+
+
+def gsr_order_cache_bins(ctx: Context, g: Gaussians, tile_start, tau: float, base_bins: int = 8,
+                         hot_bins: int = 16, stream=None) -> np.ndarray:
+    """NEXT-2b cache policy (§3.5, tau §3.6): bins per
+    tile from the tiles' mean uncertainty (computed in libgsr; SYNC)."""
+    start = np.ascontiguousarray(np.asarray(tile_start, dtype=np.int64))
+    bins = np.zeros(len(start) - 1, dtype=np.int32)
+    ctx._check(lib.gsr_order_cache_bins(ctx.handle, ctypes.byref(g.struct()), start.ctypes.data, len(bins),
+                                        float(tau), int(base_bins), int(hot_bins), bins.ctypes.data,
+                                        _stream(stream)))
+    return bins
 
 
 def gsr_composite(ctx: Context, render_rec, n: int, vals, ranges, cams, tile_partial, rgbu=None, t_final=None,

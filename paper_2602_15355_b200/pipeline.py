@@ -26,16 +26,12 @@ from .gsr import Context, Gaussians, GsrError
 CACHE_TAU, CACHE_BASE_BINS, CACHE_HOT_BINS = 0.6, 8, 16
 
 
-def cache_bins(field: Gaussians, tile_start, tau: float = CACHE_TAU) -> np.ndarray:
+def cache_bins(field: Gaussians, tile_start, tau: float = CACHE_TAU, ctx: Optional[Context] = None) -> np.ndarray:
     """NEXT-2b cache policy (§3.5, tau = 0.6 of §3.6):
     a tile whose mean per-Gaussian uncertainty exceeds tau keeps 16 cached
-    orderings, the others 8."""
-    u = field.planes[1, :, 3]
-    out = []
-    for t in range(len(tile_start) - 1):
-        m = float(u[int(tile_start[t]):int(tile_start[t + 1])].double().mean().item())
-        out.append(CACHE_HOT_BINS if m > tau else CACHE_BASE_BINS)
-    return np.asarray(out, dtype=np.int32)
+    orderings, the others 8 (gsr_order_cache_bins: one kernel, one readback)."""
+    ctx = ctx or Context(field.planes.device.index or 0)
+    return gsr.gsr_order_cache_bins(ctx, field, tile_start, tau, CACHE_BASE_BINS, CACHE_HOT_BINS)
 
 
 def tiles_per_view(cam) -> int:
@@ -222,12 +218,15 @@ class ViewScorer:
         return BatchOut(K, images)
 
     def score_views(self, cams: np.ndarray, scores_out: Optional[torch.Tensor] = None,
-                    sobel_out: Optional[torch.Tensor] = None) -> torch.Tensor:
+                    sobel_out: Optional[torch.Tensor] = None,
+                    images_out: Optional[torch.Tensor] = None) -> torch.Tensor:
         """Scores for all of ``cams`` (any count; same resolution), batches
         alternating over the slots' streams; the result is ordered back onto
         the caller's current stream.  ``sobel_out`` (optional [len(cams)]
         float tensor) also receives the NEXT-4 image term (mean Sobel
-        gradient magnitude of each rendered view, PAPER.md eq:uncert_img)."""
+        gradient magnitude of each rendered view, PAPER.md eq:uncert_img);
+        ``images_out`` (optional [len(cams)][H][W][4] float tensor) the
+        composited (r, g, b, U) maps of every view."""
         cams = gsr.cams_array(cams)
         if scores_out is None:
             scores_out = torch.empty(len(cams), dtype=torch.float32, device=self.dev)
@@ -239,6 +238,7 @@ class ViewScorer:
         for i, b0 in enumerate(range(0, len(cams), self.V)):
             b1 = min(len(cams), b0 + self.V)
             out = self._enqueue(self.slots[i % len(self.slots)], cams[b0:b1], scores_out[b0:b1],
+                                images=None if images_out is None else images_out[b0:b1],
                                 sobel_out=None if sobel_out is None else sobel_out[b0:b1])
             self.last_keys.append(out.n_keys)
         for s in self.slots:

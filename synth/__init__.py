@@ -352,12 +352,6 @@ def config4_tiles(n_per_tile: int = 500_000, lod: bool = False):
     return start, centres
 
 
-def tile_mean_uncertainty(field, tile_start) -> np.ndarray:
-    """Mean per-Gaussian uncertainty of each tile (the cache policy input)."""
-    u = field.planes[1, :, 3].astype(np.float64)
-    return np.array([u[tile_start[t]:tile_start[t + 1]].mean() for t in range(len(tile_start) - 1)])
-
-
 def random_lod(rng, n: int, levels: int = 4, thresholds=(1.0, 2.0, 3.0), delta: float = 0.3,
                centre_range: float = 1.5) -> LodData:
     """Random tile centres and levels for parity tests."""

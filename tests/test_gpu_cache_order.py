@@ -78,9 +78,34 @@ def test_flyover_scorer_cached_vs_oracle(ctx):
     from paper_2602_15355_b200.pipeline import ViewScorer
     fld = synth.gen_config4_field(4_000)
     start, centres = synth.config4_tiles(4_000)
-    bins = [co.bins_for(u) for u in synth.tile_mean_uncertainty(fld, start)]
+    bins = [co.bins_for(u) for u in co.tile_mean_uncertainty(fld, start)]
     cams = synth.with_resolution(synth.flyover_cameras(64, 1920, 1080, 1500.0)[::8], 480, 270, 375.0)
     sc = ViewScorer(to_dev(fld), batch_views=4, order_tiles=(start, bins, centres))
     got = sc.score_views(cams).cpu().numpy()
     ref = np.array([co.render_view_cached(fld, c, start, bins, centres)["score"] for c in cams])
     np.testing.assert_allclose(got, ref, rtol=1e-4)
+
+
+def test_cache_policy_bins_in_libgsr(ctx):
+    """gsr_order_cache_bins (pipeline.cache_bins) = the oracle's policy
+    (§3.5, tau = 0.6): per tile, 16 bins if its mean
+    uncertainty exceeds tau, else 8 -- on the configs[3] tiles, on tiles made
+    hot / cold on purpose, and for a tau just below / above one tile's mean."""
+    from paper_2602_15355_b200 import gsr
+    from paper_2602_15355_b200.pipeline import cache_bins
+    fld = synth.gen_config4_field(4_000)
+    start, _ = synth.config4_tiles(4_000)
+    planes = fld.planes.copy()
+    planes[1, start[1]:start[2], 3] = 0.9  # hot tile
+    planes[1, start[2]:start[3], 3] = 0.1  # cold tile
+    fld = synth.GaussianField(planes, fld.sh_degree)
+    G = to_dev(fld)
+    means = co.tile_mean_uncertainty(fld, start)
+    want = np.array([co.bins_for(u) for u in means], np.int32)
+    got = cache_bins(G, start, ctx=ctx)
+    assert np.array_equal(got, want) and got[1] == 16 and got[2] == 8
+    for tau, hot in ((means[0] * (1 - 1e-6), 16), (means[0] * (1 + 1e-6), 8)):
+        b = gsr.gsr_order_cache_bins(ctx, G, start, float(tau))
+        assert b[0] == hot and np.array_equal(b, [co.bins_for(u, float(np.float32(tau))) for u in means])
+    with pytest.raises(gsr.GsrError):
+        gsr.gsr_order_cache_bins(ctx, G, np.asarray(start)[:-1], 0.6)  # does not cover [0, n)

@@ -58,7 +58,7 @@ def test_cached_vs_exact_fidelity_on_flyover():
     bins (configs[3] geometry, 4,000 Gaussians per tile, 3 views)."""
     fld = synth.gen_config4_field(4_000)
     start, centres = synth.config4_tiles(4_000)
-    bins = [co.bins_for(u) for u in synth.tile_mean_uncertainty(fld, start)]
+    bins = [co.bins_for(u) for u in co.tile_mean_uncertainty(fld, start)]
     assert set(bins) == {8}
     cams = synth.with_resolution(synth.flyover_cameras(64, 1920, 1080, 1500.0)[::21], 480, 270, 375.0)
     for cam in cams:
