@@ -78,15 +78,9 @@ gsr_status gsr_create(gsr_ctx** out, int device) {
   gsr_ctx* c = new gsr_ctx();
   c->device = device;
   cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
-  if (const char* v = std::getenv("GSR_COMPOSITE")) c->composite_variant = std::atoi(v);
-  if (const char* v = std::getenv("GSR_SORT")) c->sort_variant = std::atoi(v);
-  if (const char* v = std::getenv("GSR_STAGES")) c->composite_stages = std::atoi(v);
-  if (const char* v = std::getenv("GSR_PIX")) c->composite_pix = std::atoi(v);
-  if (const char* v = std::getenv("GSR_KPT")) c->sort_kpt32 = std::atoi(v);
   if (const char* v = std::getenv("GSR_DKEY64")) c->depth_keys64 = std::atoi(v) != 0;
   if (const char* v = std::getenv("GSR_BWRED")) c->bw_reduce = std::atoi(v);
   if (const char* v = std::getenv("GSR_BWNW")) c->bw_warps = std::atoi(v);
-  if (const char* v = std::getenv("GSR_K6ORDER")) c->k6_order = std::atoi(v) != 0;
   if (const char* v = std::getenv("GSR_PACK")) c->pack_tile_keys = std::atoi(v);
   if (const char* v = std::getenv("GSR_TSORT"))
     c->tile_sort_mode = std::string(v) == "radix" ? 2 : (std::string(v) == "cs" ? 1 : 0);

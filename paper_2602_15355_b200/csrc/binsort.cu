@@ -288,14 +288,10 @@ __global__ void __launch_bounds__(256) hist_u64(const uint64_t* __restrict__ key
 //   MODE 1: tile sort final pass (KeyT = u32 key = view*tpv + tile): write
 //           vals_out and, if keys64 != null, the full 64-bit key
 //           (key << 32) | depth_plane[view * nper + g].
-// LB = 0: decoupled look-back (classic onesweep: lookback = flag words, ctr =
-//         dynamic block ids).  LB = 1: the per-(digit, tile) output offsets were
-//         precomputed by rs_upsweep + rs_scan (lookback = gofs[256][ntiles]),
-//         so a tile needs no inter-block communication at all.
 #ifndef OS_MINB12
 #define OS_MINB12 4  // 12-key tiles: 4 blocks per SM (64 registers, small spills) measured +0.4 % over 3
 #endif
-template <typename KeyT, int KPT, int MODE, int LB = 0>
+template <typename KeyT, int KPT, int MODE>
 __global__ void __launch_bounds__(256, (KPT <= 8 ? 4 : OS_MINB12)) onesweep(const KeyT* __restrict__ kin, const uint32_t* __restrict__ vin,
                                                 KeyT* __restrict__ kout, uint32_t* __restrict__ vout, uint32_t n,
                                                 int shift, int nbits, const uint32_t* __restrict__ base,
@@ -315,7 +311,7 @@ __global__ void __launch_bounds__(256, (KPT <= 8 ? 4 : OS_MINB12)) onesweep(cons
   __shared__ uint32_t s_start[256], s_gbase[256], s_cnt[256], s_wsum[W];
   __shared__ uint32_t s_bid;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (tid == 0) s_bid = LB ? blockIdx.x : atomicAdd(ctr, 1u);
+  if (tid == 0) s_bid = atomicAdd(ctr, 1u);
   for (int i = tid; i < W * 256; i += B) (&u.hist[0][0])[i] = 0;
   s_cnt[tid] = 0;
   __syncthreads();
@@ -338,7 +334,7 @@ __global__ void __launch_bounds__(256, (KPT <= 8 ? 4 : OS_MINB12)) onesweep(cons
   constexpr int WIN = 8;
   uint32_t win[WIN];
   uint32_t early_total = 0;
-  if (!LB) {
+  {
 #pragma unroll
     for (int k = 0; k < KPT; ++k) {
       const int64_t idx = wbase + k * 32 + lane;
@@ -380,9 +376,7 @@ __global__ void __launch_bounds__(256, (KPT <= 8 ? 4 : OS_MINB12)) onesweep(cons
     }
     uint32_t* my = lookback + (size_t)bid * 256 + d;
     uint32_t excl = 0;
-    if (LB) {
-      excl = lookback[(size_t)d * gridDim.x + bid] - base[d];  // gofs - digit base
-    } else if (bid != 0) {
+    if (bid != 0) {
       // windowed decoupled look-back: WIN predecessors per round trip
       int64_t j = (int64_t)bid - 1;
       while (true) {
@@ -472,326 +466,6 @@ __global__ void __launch_bounds__(256, (KPT <= 8 ? 4 : OS_MINB12)) onesweep(cons
       }
     }
   }
-}
-
-// ---------------------------------------------------------------------------
-// Reduce-then-scan support for onesweep<..., LB = 1>:
-//   rs_upsweep: per-tile digit histogram -> counts[d][tile] (digit-major)
-//   rs_scan:    gofs[d][tile] = base[d] + sum_{t' < t} counts[d][t'] (in place)
-// Traffic: +4 B/key (u32 keys) to read the keys once more, but no serial
-// inter-tile chain: measured, the decoupled look-back's walk length grew with
-// the ~450 co-resident tiles and dominated the pass.
-template <typename KeyT, int KPT>
-__global__ void __launch_bounds__(256) rs_upsweep(const KeyT* __restrict__ kin, uint32_t n, int shift, int nbits,
-                                                  uint32_t* __restrict__ counts) {
-  constexpr int TILE = 256 * KPT;
-  __shared__ uint32_t h[8][256];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  for (int i = tid; i < 8 * 256; i += 256) (&h[0][0])[i] = 0;
-  __syncthreads();
-  const uint32_t mask = (nbits >= 32) ? 0xffffffffu : ((1u << nbits) - 1);
-  const int64_t wbase = (int64_t)blockIdx.x * TILE + (int64_t)warp * (KPT * 32);
-#pragma unroll
-  for (int k = 0; k < KPT; ++k) {
-    const int64_t idx = wbase + k * 32 + lane;
-    if (idx < (int64_t)n) atomicAdd(&h[warp][(uint32_t)(kin[idx] >> shift) & mask], 1u);
-  }
-  __syncthreads();
-  uint32_t c = 0;
-#pragma unroll
-  for (int w = 0; w < 8; ++w) c += h[w][tid];
-  counts[(size_t)tid * gridDim.x + blockIdx.x] = c;
-}
-
-__global__ void __launch_bounds__(1024) rs_scan(uint32_t* __restrict__ counts, uint32_t ntiles,
-                                                const uint32_t* __restrict__ base) {
-  __shared__ uint32_t s_w[32];
-  __shared__ uint32_t s_carry;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  uint32_t* col = counts + (size_t)blockIdx.x * ntiles;
-  if (tid == 0) s_carry = base[blockIdx.x];
-  __syncthreads();
-  constexpr int IT = 4;
-  for (uint32_t c0 = 0; c0 < ntiles; c0 += 1024 * IT) {
-    uint32_t v[IT], sum = 0;
-    const uint32_t t0 = c0 + tid * IT;
-#pragma unroll
-    for (int k = 0; k < IT; ++k) {
-      v[k] = t0 + k < ntiles ? col[t0 + k] : 0u;
-      sum += v[k];
-    }
-    const uint32_t inc = warp_incl_scan<uint32_t>(sum);
-    if (lane == 31) s_w[warp] = inc;
-    __syncthreads();
-    if (warp == 0) {
-      const uint32_t wv = s_w[lane];
-      s_w[lane] = warp_incl_scan<uint32_t>(wv) - wv;
-    }
-    __syncthreads();
-    uint32_t run = s_carry + s_w[warp] + inc - sum;
-#pragma unroll
-    for (int k = 0; k < IT; ++k) {
-      if (t0 + k < ntiles) col[t0 + k] = run;
-      run += v[k];
-    }
-    __syncthreads();
-    if (tid == 1023) s_carry = run;
-    __syncthreads();
-  }
-}
-
-// ---------------------------------------------------------------------------
-// Persistent onesweep pass (the production variant).  grid = resident CTAs;
-// each CTA takes tiles in dynamic order (atomic counter) and, while it ranks
-// tile t, a TMA bulk copy (cp.async.bulk) already streams its next tile's keys
-// and values into the other half of a double buffer, completing on an
-// mbarrier.  Keys are ranked straight out of shared memory (no key registers),
-// which leaves room for 3 CTAs / SM.  Forward progress of the look-back holds
-// because every CTA processes its tiles in increasing id order: the smallest
-// unfinished tile is always being processed by its owner.
-__device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void mbar_init1(uint64_t* b) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(b)) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_tx1(uint64_t* b, uint32_t tx) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(b)), "r"(tx) : "memory");
-}
-__device__ __forceinline__ void mbar_wait1(uint64_t* b, uint32_t parity) {
-  uint32_t ok = 0;
-  while (!ok) {
-    asm volatile(
-        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
-        : "=r"(ok)
-        : "r"(smem_addr(b)), "r"(parity)
-        : "memory");
-  }
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                   smem_addr(dst)),
-               "l"(src), "r"(bytes), "r"(smem_addr(bar))
-               : "memory");
-}
-
-template <typename KeyT, int KPT>
-struct PSmem {
-  static constexpr int TILE = 256 * KPT;
-  KeyT rk[2][TILE];
-  uint32_t rv[2][TILE];
-  union {
-    uint32_t hist[8][256];
-    struct {
-      KeyT k[TILE];
-      uint32_t v[TILE];
-    } st;
-  } u;
-  uint32_t start[256], gbase[256], cnt[256], wsum[8];
-  uint32_t tile[2];
-  uint64_t full[2];
-};
-
-template <typename KeyT, int KPT>
-__device__ __forceinline__ void p_issue(PSmem<KeyT, KPT>& S, int buf, uint32_t t, const KeyT* kin,
-                                        const uint32_t* vin, uint32_t n) {
-  constexpr int TILE = PSmem<KeyT, KPT>::TILE;
-  const uint64_t first = (uint64_t)t * TILE;
-  const uint32_t cnt = (uint32_t)min((uint64_t)TILE, (uint64_t)n - first);
-  const uint32_t kb = (cnt * (uint32_t)sizeof(KeyT)) & ~15u, vb = (cnt * 4u) & ~15u;
-  // the last tile's ragged tail (< 16 B per array) is loaded by the threads
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-  mbar_arrive_tx1(&S.full[buf], kb + vb);
-  if (kb) bulk_g2s(S.rk[buf], kin + first, kb, &S.full[buf]);
-  if (vb) bulk_g2s(S.rv[buf], vin + first, vb, &S.full[buf]);
-}
-
-template <typename KeyT, int KPT, int MODE>
-__global__ void __launch_bounds__(256) onesweep_p(const KeyT* __restrict__ kin, const uint32_t* __restrict__ vin,
-                                                  KeyT* __restrict__ kout, uint32_t* __restrict__ vout, uint32_t n,
-                                                  int shift, int nbits, const uint32_t* __restrict__ base,
-                                                  uint32_t* __restrict__ lookback, uint32_t* __restrict__ ctr,
-                                                  uint64_t* __restrict__ keys64,
-                                                  const uint32_t* __restrict__ depth_plane, uint32_t tpv,
-                                                  int64_t nper) {
-  using SM = PSmem<KeyT, KPT>;
-  constexpr int B = 256, W = 8, TILE = SM::TILE;
-  extern __shared__ __align__(128) unsigned char p_raw[];
-  SM& S = *reinterpret_cast<SM*>(p_raw);
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const uint32_t ntiles = (n + TILE - 1) / TILE;
-  const uint32_t mask = (nbits >= 32) ? 0xffffffffu : ((1u << nbits) - 1);
-  if (tid == 0) {
-    mbar_init1(&S.full[0]);
-    mbar_init1(&S.full[1]);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    const uint32_t t0 = atomicAdd(ctr, 1u);
-    S.tile[0] = t0;
-    if (t0 < ntiles) p_issue<KeyT, KPT>(S, 0, t0, kin, vin, n);
-  }
-  __syncthreads();
-  const uint32_t lt = (1u << lane) - 1;
-  for (uint32_t it = 0;; ++it) {
-    const int buf = it & 1;
-    const uint32_t t = S.tile[buf];
-    if (t >= ntiles) break;
-    if (tid == 0) {  // prefetch the next tile into the other buffer (read by the previous iteration)
-      const uint32_t t1 = atomicAdd(ctr, 1u);
-      S.tile[buf ^ 1] = t1;
-      if (t1 < ntiles) p_issue<KeyT, KPT>(S, buf ^ 1, t1, kin, vin, n);
-    }
-    const uint64_t first = (uint64_t)t * TILE;
-    const uint32_t cnt = (uint32_t)min((uint64_t)TILE, (uint64_t)n - first);
-    for (int i = tid; i < W * 256; i += B) (&S.u.hist[0][0])[i] = 0;
-    S.cnt[tid] = 0;
-    {  // ragged tail of the last tile
-      const uint32_t kt = ((cnt * (uint32_t)sizeof(KeyT)) & ~15u) / sizeof(KeyT), vt = ((cnt * 4u) & ~15u) / 4u;
-      if ((uint32_t)tid < cnt - kt) S.rk[buf][kt + tid] = kin[first + kt + tid];
-      if ((uint32_t)tid < cnt - vt) S.rv[buf][vt + tid] = vin[first + vt + tid];
-    }
-    mbar_wait1(&S.full[buf], (it >> 1) & 1);
-    __syncthreads();
-    const KeyT* rk = S.rk[buf];
-    const int wl = warp * (KPT * 32);
-    // (1) early digit counts of the whole tile (shared-memory atomics), so the
-    //     aggregate is published and the look-back loads are in flight while
-    //     the warps rank their keys
-#pragma unroll
-    for (int k = 0; k < KPT; ++k) {
-      const int li = wl + k * 32 + lane;
-      if ((uint32_t)li < cnt) atomicAdd(&S.cnt[(uint32_t)(rk[li] >> shift) & mask], 1u);
-    }
-    __syncthreads();
-    const uint32_t total = S.cnt[tid];
-    uint32_t* my = lookback + (size_t)t * 256 + tid;
-    st_word(my, (t == 0 ? DG_INC : DG_AGG) | total);
-    constexpr int WIN = 8;  // predecessors read per look-back round trip
-    uint32_t win[WIN];
-#pragma unroll
-    for (int i = 0; i < WIN; ++i) {
-      const int64_t j = (int64_t)t - 1 - i;
-      win[i] = j >= 0 ? ld_word(lookback + (size_t)j * 256 + tid) : DG_INC;
-    }
-    // (2) stable warp-level ranking (match_any) into per-warp histograms
-    uint32_t rank[KPT];
-#pragma unroll
-    for (int k = 0; k < KPT; ++k) {
-      const int li = wl + k * 32 + lane;
-      const bool valid = (uint32_t)li < cnt;
-      const uint32_t d = valid ? (uint32_t)(rk[li] >> shift) & mask : 0u;
-      const uint32_t peers = match_digit8(valid, d);
-      const uint32_t r = __popc(peers & lt);
-      uint32_t pre = 0;
-      if (valid) pre = S.u.hist[warp][d];
-      __syncwarp();
-      if (valid && r == 0) S.u.hist[warp][d] = pre + __popc(peers);
-      __syncwarp();
-      rank[k] = pre + r;
-    }
-    __syncthreads();
-    {
-      const int d = tid;
-      uint32_t run = 0;
-#pragma unroll
-      for (int w = 0; w < W; ++w) {
-        const uint32_t c = S.u.hist[w][d];
-        S.u.hist[w][d] = run;
-        run += c;
-      }
-      // (3) finish the windowed decoupled look-back
-      uint32_t excl = 0;
-      if (t != 0) {
-        int64_t j = (int64_t)t - 1;
-        while (true) {
-          int i = 0;
-          bool done = false;
-#pragma unroll
-          for (; i < WIN; ++i) {
-            const uint32_t f = win[i] >> 30;
-            if (f == 0) break;
-            excl += win[i] & DG_VAL;
-            if (f == 2) {
-              done = true;
-              break;
-            }
-          }
-          if (done) break;
-          j -= i;  // consumed i aggregates; re-read from the first word not yet ready
-#pragma unroll
-          for (int q = 0; q < WIN; ++q) {
-            const int64_t jj = j - q;
-            win[q] = jj >= 0 ? ld_word(lookback + (size_t)jj * 256 + d) : DG_INC;
-          }
-        }
-        st_word(my, DG_INC | (excl + total));
-      }
-      const uint32_t inc = warp_incl_scan<uint32_t>(total);
-      if (lane == 31) S.wsum[warp] = inc;
-      __syncthreads();
-      uint32_t off = 0;
-#pragma unroll
-      for (int w = 0; w < W; ++w) off += (w < warp) ? S.wsum[w] : 0u;
-      const uint32_t start = off + inc - total;
-      S.start[d] = start;
-      S.gbase[d] = base[d] + excl - start;
-    }
-    __syncthreads();
-#pragma unroll
-    for (int k = 0; k < KPT; ++k) {
-      const int li = wl + k * 32 + lane;
-      if ((uint32_t)li < cnt) {
-        const uint32_t d = (uint32_t)(rk[li] >> shift) & mask;
-        rank[k] += S.start[d] + S.u.hist[warp][d];
-      }
-    }
-    __syncthreads();  // hist (aliased with the stage) fully consumed
-#pragma unroll
-    for (int k = 0; k < KPT; ++k) {
-      const int li = wl + k * 32 + lane;
-      if ((uint32_t)li < cnt) {
-        S.u.st.k[rank[k]] = rk[li];
-        S.u.st.v[rank[k]] = S.rv[buf][li];
-      }
-    }
-    __syncthreads();
-    for (int i = tid; i < (int)cnt; i += B) {
-      const KeyT kk = S.u.st.k[i];
-      const uint32_t vv = S.u.st.v[i];
-      const uint32_t d = (uint32_t)(kk >> shift) & mask;
-      const uint32_t o = S.gbase[d] + i;
-      if (MODE == 0) {
-        kout[o] = kk;
-        vout[o] = vv;
-      } else {
-        vout[o] = vv;
-        if (keys64) {
-          const uint32_t k32 = (uint32_t)kk;
-          const uint32_t view = k32 / tpv;
-          keys64[o] = ((uint64_t)k32 << 32) | __ldg(depth_plane + (int64_t)view * nper + vv);
-        }
-      }
-    }
-    __syncthreads();  // stage and this buffer free for the next iteration / prefetch
-  }
-}
-
-// Launch one pass with the persistent kernel (grid = resident CTAs).
-template <typename KeyT, int KPT, int MODE>
-cudaError_t launch_pass(const KeyT* kin, const uint32_t* vin, KeyT* kout, uint32_t* vout, uint32_t n, int shift,
-                        int nbits, const uint32_t* base, uint32_t* lookback, uint32_t* ctr, uint64_t* keys64,
-                        const uint32_t* depth_plane, uint32_t tpv, int64_t nper, int num_sms, cudaStream_t st) {
-  static int per_sm = 0;
-  const size_t smem = sizeof(PSmem<KeyT, KPT>);
-  if (per_sm == 0) {
-    cudaFuncSetAttribute(onesweep_p<KeyT, KPT, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaFuncSetAttribute(onesweep_p<KeyT, KPT, MODE>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, onesweep_p<KeyT, KPT, MODE>, 256, smem);
-    if (per_sm < 1) per_sm = 1;
-  }
-  const uint32_t ntiles = (n + PSmem<KeyT, KPT>::TILE - 1) / PSmem<KeyT, KPT>::TILE;
-  const uint32_t grid = std::min<uint32_t>(ntiles, (uint32_t)(per_sm * num_sms));
-  if (grid == 0) return cudaSuccess;
-  onesweep_p<KeyT, KPT, MODE><<<grid, 256, smem, st>>>(kin, vin, kout, vout, n, shift, nbits, base, lookback, ctr,
-                                                        keys64, depth_plane, tpv, nper);
-  return cudaGetLastError();
 }
 
 // ---------------------------------------------------------------------------
@@ -1453,63 +1127,27 @@ int bits_for(uint64_t count) {  // ceil(log2(count)), 0 for count <= 1
 }
 
 constexpr int KPT64 = 12;  // onesweep u64 keys: 3072 keys per block
-constexpr int PKPT64 = 8;  // persistent onesweep u64 keys: 2048 keys per tile
-constexpr int PKPT32 = 12; // persistent onesweep u32 keys: 3072 keys per tile
 constexpr int KPT32 = 12;  // onesweep u32 keys: 3072 keys per block
 
-// Sort-pass variants (gsr_ctx::sort_variant, env GSR_SORT):
-//   1  onesweep, one tile per block, decoupled look-back (default: best with 2 streams)
-//   2  persistent onesweep, TMA-fed double buffer, windowed look-back
-//   3  reduce-then-scan: rs_upsweep + rs_scan + onesweep<LB=1> scatter
 template <typename KeyT>
-size_t pass_tile(int variant, int kpt32 = KPT32) {
-  if (variant == 2) return 256 * (sizeof(KeyT) == 8 ? PKPT64 : PKPT32);
-  return 256 * (sizeof(KeyT) == 8 ? KPT64 : kpt32);
+constexpr size_t pass_tile() {
+  return 256 * (sizeof(KeyT) == 8 ? KPT64 : KPT32);
 }
 
-template <typename KeyT, int K, int MODE>
-cudaError_t launch_onesweep(int variant, uint32_t nt, const KeyT* kin, const uint32_t* vin, KeyT* kout,
-                            uint32_t* vout, uint32_t n, int shift, int nbits, const uint32_t* base, uint32_t* region,
-                            uint32_t* ctr, uint64_t* keys64, const uint32_t* depth_plane, uint32_t tpv, int64_t nper,
-                            cudaStream_t st) {
-  if (variant == 1) {
-    onesweep<KeyT, K, MODE, 0><<<nt, 256, 0, st>>>(kin, vin, kout, vout, n, shift, nbits, base, region, ctr, keys64,
-                                                   depth_plane, tpv, nper);
-    return cudaGetLastError();
-  }
-  rs_upsweep<KeyT, K><<<nt, 256, 0, st>>>(kin, n, shift, nbits, region);
-  rs_scan<<<1u << (nbits < 8 ? nbits : 8), 1024, 0, st>>>(region, nt, base);
-  onesweep<KeyT, K, MODE, 1><<<nt, 256, 0, st>>>(kin, vin, kout, vout, n, shift, nbits, base, region, ctr, keys64,
-                                                 depth_plane, tpv, nper);
+// One stable LSD onesweep pass by digit (key >> shift) & (2^nbits - 1).
+// `region` holds ceil(n / pass_tile) * 256 zero-initialised look-back words;
+// `ctr` one zero-initialised counter (dynamic block ids).
+template <typename KeyT, int MODE>
+cudaError_t run_pass(const KeyT* kin, const uint32_t* vin, KeyT* kout, uint32_t* vout, uint32_t n, int shift, int nbits,
+                     const uint32_t* base, uint32_t* region, uint32_t* ctr, uint64_t* keys64,
+                     const uint32_t* depth_plane, uint32_t tpv, int64_t nper, cudaStream_t st) {
+  if (n == 0) return cudaSuccess;
+  constexpr int K = sizeof(KeyT) == 8 ? KPT64 : KPT32;
+  const uint32_t nt = (uint32_t)((n + pass_tile<KeyT>() - 1) / pass_tile<KeyT>());
+  onesweep<KeyT, K, MODE><<<nt, 256, 0, st>>>(kin, vin, kout, vout, n, shift, nbits, base, region, ctr, keys64,
+                                              depth_plane, tpv, nper);
   return cudaGetLastError();
 }
-
-// One stable LSD pass by digit (key >> shift) & (2^nbits - 1).  `region` holds
-// ceil(n / pass_tile) * 256 zero-initialised words (look-back flags or the
-// per-(digit, tile) offsets); `ctr` one zero-initialised counter.
-template <typename KeyT, int MODE>
-cudaError_t run_pass(int variant, int num_sms, const KeyT* kin, const uint32_t* vin, KeyT* kout, uint32_t* vout,
-                     uint32_t n, int shift, int nbits, const uint32_t* base, uint32_t* region, uint32_t* ctr,
-                     uint64_t* keys64, const uint32_t* depth_plane, uint32_t tpv, int64_t nper, cudaStream_t st,
-                     int kpt32 = KPT32) {
-  if (n == 0) return cudaSuccess;
-  constexpr int PK = sizeof(KeyT) == 8 ? PKPT64 : PKPT32;
-  const uint32_t nt = (uint32_t)((n + pass_tile<KeyT>(variant, kpt32) - 1) / pass_tile<KeyT>(variant, kpt32));
-  if (variant == 2)
-    return launch_pass<KeyT, PK, MODE>(kin, vin, kout, vout, n, shift, nbits, base, region, ctr, keys64, depth_plane,
-                                       tpv, nper, num_sms, st);
-  if constexpr (sizeof(KeyT) == 8) {
-    return launch_onesweep<KeyT, KPT64, MODE>(variant, nt, kin, vin, kout, vout, n, shift, nbits, base, region, ctr,
-                                              keys64, depth_plane, tpv, nper, st);
-  } else {
-    if (kpt32 == 8)
-      return launch_onesweep<KeyT, 8, MODE>(variant, nt, kin, vin, kout, vout, n, shift, nbits, base, region, ctr,
-                                            keys64, depth_plane, tpv, nper, st);
-    return launch_onesweep<KeyT, KPT32, MODE>(variant, nt, kin, vin, kout, vout, n, shift, nbits, base, region, ctr,
-                                              keys64, depth_plane, tpv, nper, st);
-  }
-}
-inline int pass_launches(int variant) { return variant == 3 ? 3 : 1; }
 
 size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
@@ -1522,10 +1160,7 @@ static gsr_status sort_u64_passes(gsr_ctx* ctx, const uint64_t* kin, const uint3
                                   int end_bit, const uint32_t* base, uint32_t* region, uint32_t* ctrs,
                                   cudaStream_t st) {
   const int passes = (end_bit - begin_bit + 7) / 8;
-  // the persistent variant streams tiles with TMA bulk copies: 16-B aligned buffers only
-  const bool aligned = ((((uintptr_t)kin) | ((uintptr_t)vin) | ((uintptr_t)kout) | ((uintptr_t)vout)) & 15) == 0;
-  const int variant = (ctx->sort_variant == 2 && !aligned) ? 3 : ctx->sort_variant;
-  const size_t nb = (size_t)((n + pass_tile<uint64_t>(variant) - 1) / pass_tile<uint64_t>(variant));
+  const size_t nb = (size_t)((n + pass_tile<uint64_t>() - 1) / pass_tile<uint64_t>());
   // choose buffers so that the last pass lands in kout
   const uint64_t* ci = kin;
   const uint32_t* cv = vin;
@@ -1535,7 +1170,7 @@ static gsr_status sort_u64_passes(gsr_ctx* ctx, const uint64_t* kin, const uint3
     uint32_t* vo = to_out ? vout : vtmp;
     const int sh = begin_bit + 8 * p;
     const int nbits = std::min(8, end_bit - sh);
-    cudaError_t e = run_pass<uint64_t, 0>(variant, ctx->num_sms, ci, cv, ko, vo, (uint32_t)n, sh, nbits,
+    cudaError_t e = run_pass<uint64_t, 0>(ci, cv, ko, vo, (uint32_t)n, sh, nbits,
                                           base + 256 * p, region + (size_t)p * nb * 256, ctrs + p, nullptr, nullptr,
                                           0, 0, st);
     if (e != cudaSuccess) return check_cuda(ctx, e, "sort pass u64");
@@ -1562,7 +1197,7 @@ extern "C" gsr_status gsr_sort_pairs_u64(gsr_ctx* ctx, const uint64_t* keys_in, 
   if (n == 0) return GSR_OK;
   cudaStream_t st = (cudaStream_t)stream;
   const int passes = (end_bit - begin_bit + 7) / 8;
-  const size_t nb = (size_t)((n + 256 * PKPT64 - 1) / (256 * PKPT64));  // >= every variant's tile count
+  const size_t nb = (size_t)((n + pass_tile<uint64_t>() - 1) / pass_tile<uint64_t>());
   void *kt, *vt, *hs, *lb;
   gsr_status s;
   if ((s = ensure(ctx, S_SORTK, n * 8, &kt)) != GSR_OK) return s;
@@ -1578,7 +1213,7 @@ extern "C" gsr_status gsr_sort_pairs_u64(gsr_ctx* ctx, const uint64_t* keys_in, 
   if ((s = check_cuda(ctx, cudaMemsetAsync(lb, 0, lb_bytes, st), "memset")) != GSR_OK) return s;
   const int hb = (int)std::min<int64_t>((n + 255) / 256, (int64_t)ctx->num_sms * 8);
   StageScope scope(ctx, GSR_STAGE_SORT_U64, st);
-  account(ctx, GSR_STAGE_SORT_U64, 2 + passes * pass_launches(ctx->sort_variant), 8.0 * n + 24.0 * passes * n);
+  account(ctx, GSR_STAGE_SORT_U64, 2 + passes, 8.0 * n + 24.0 * passes * n);
   hist_u64<<<hb, 256, 0, st>>>(keys_in, n, begin_bit, passes, end_bit, hist);
   scan_hist<<<1, 256, 0, st>>>(hist, base, passes);
   if ((s = check_cuda(ctx, cudaGetLastError(), "hist")) != GSR_OK) return s;
@@ -1708,10 +1343,8 @@ static gsr_status bin_sort_impl(gsr_ctx* ctx, const uint32_t* bin_rec, int64_t n
   if ((s = ensure(ctx, S_TVAL_A, 2 * align_up(K * 4), &tva)) != GSR_OK) return s;
   tvb = (char*)tva + align_up(K * 4);
   if ((s = ensure(ctx, S_COUNTS, T * 4, &cnt)) != GSR_OK) return s;
-  const int variant = ctx->sort_variant;
-  const int kpt32 = ctx->sort_kpt32;
-  const size_t dtile = wide ? pass_tile<uint64_t>(variant) : pass_tile<uint32_t>(variant, kpt32);
-  const size_t ttile = pass_tile<uint32_t>(variant, kpt32);
+  const size_t dtile = wide ? pass_tile<uint64_t>() : pass_tile<uint32_t>();
+  const size_t ttile = pass_tile<uint32_t>();
   const size_t nbd = (size_t)((nvis + dtile - 1) / dtile);
   const size_t nb3 = (size_t)((nvis + K3_TILE - 1) / K3_TILE);
   const size_t nbt = (size_t)((K + ttile - 1) / ttile);
@@ -1743,19 +1376,18 @@ static gsr_status bin_sort_impl(gsr_ctx* ctx, const uint32_t* bin_rec, int64_t n
       void* ko = (p % 2 == 0) ? dkb : dka;
       uint32_t* vo = (p % 2 == 0) ? (uint32_t*)dvb : (uint32_t*)dva;
       const int sh = 8 * p;
-      cudaError_t e = wide ? run_pass<uint64_t, 0>(variant, ctx->num_sms, (const uint64_t*)ck, cvv, (uint64_t*)ko, vo,
+      cudaError_t e = wide ? run_pass<uint64_t, 0>((const uint64_t*)ck, cvv, (uint64_t*)ko, vo,
                                                    (uint32_t)nvis, sh, std::min(8, kbits - sh), dbase + 256 * p,
                                                    lbd + (size_t)p * nbd * 256, ctrs + p, nullptr, nullptr, 0, 0, st)
-                           : run_pass<uint32_t, 0>(variant, ctx->num_sms, (const uint32_t*)ck, cvv, (uint32_t*)ko, vo,
+                           : run_pass<uint32_t, 0>((const uint32_t*)ck, cvv, (uint32_t*)ko, vo,
                                                    (uint32_t)nvis, sh, 8, dbase + 256 * p,
-                                                   lbd + (size_t)p * nbd * 256, ctrs + p, nullptr, nullptr, 0, 0, st,
-                                                   kpt32);
+                                                   lbd + (size_t)p * nbd * 256, ctrs + p, nullptr, nullptr, 0, 0, st);
       if ((s = check_cuda(ctx, e, "depth sort pass")) != GSR_OK) return s;
       ck = ko;
       cvv = vo;
     }
     stage_end(ctx, spd, st);
-    account(ctx, GSR_STAGE_DEPTH_SORT, 1 + dpasses * pass_launches(variant), (wide ? 24.0 : 16.0) * dpasses * nvis);
+    account(ctx, GSR_STAGE_DEPTH_SORT, 1 + dpasses, (wide ? 24.0 : 16.0) * dpasses * nvis);
     if ((s = check_cuda(ctx, cudaGetLastError(), "depth sort")) != GSR_OK) return s;
   }
 
@@ -1843,13 +1475,13 @@ static gsr_status bin_sort_impl(gsr_ctx* ctx, const uint32_t* bin_rec, int64_t n
     uint32_t* lbp = lbt + (size_t)p * nbt * 256;
     cudaError_t e;
     if (p == tpasses - 1) {
-      e = run_pass<uint32_t, 1>(variant, ctx->num_sms, tk, tv, nullptr, vals, (uint32_t)K, sh, nbits,
-                                tbase + 256 * p, lbp, ctrs + 6 + p, keys, p_depth, (uint32_t)tpv, n, st, kpt32);
+      e = run_pass<uint32_t, 1>(tk, tv, nullptr, vals, (uint32_t)K, sh, nbits, tbase + 256 * p, lbp, ctrs + 6 + p,
+                                keys, p_depth, (uint32_t)tpv, n, st);
     } else {
       uint32_t* ko = (p % 2 == 0) ? (uint32_t*)tkb : (uint32_t*)tka;
       uint32_t* vo = (p % 2 == 0) ? (uint32_t*)tvb : (uint32_t*)tva;
-      e = run_pass<uint32_t, 0>(variant, ctx->num_sms, tk, tv, ko, vo, (uint32_t)K, sh, nbits, tbase + 256 * p, lbp,
-                                ctrs + 6 + p, nullptr, nullptr, 0, 0, st, kpt32);
+      e = run_pass<uint32_t, 0>(tk, tv, ko, vo, (uint32_t)K, sh, nbits, tbase + 256 * p, lbp, ctrs + 6 + p, nullptr,
+                                nullptr, 0, 0, st);
       tk = ko;
       tv = vo;
     }
@@ -1858,7 +1490,7 @@ static gsr_status bin_sort_impl(gsr_ctx* ctx, const uint32_t* bin_rec, int64_t n
   stage_end(ctx, sp, st);
   // each pass reads 8 B/key; intermediate passes write 8 B/key, the last writes
   // the 4-B values (+ 8-B keys when asked)
-  account(ctx, GSR_STAGE_TILE_SORT, tpasses * pass_launches(variant),
+  account(ctx, GSR_STAGE_TILE_SORT, tpasses,
           16.0 * (tpasses - 1) * K + (12.0 + (keys ? 8.0 : 0.0)) * K);
   if ((s = check_cuda(ctx, cudaGetLastError(), "tile sort")) != GSR_OK) return s;
 

@@ -138,8 +138,7 @@ enum Slot {
   S_SELECT2,                                // NEXT-1 per-chunk partial sums
   S_GRAD2D,                                 // NEXT-3 per-(view, g) 2D gradients
   S_CSH, S_CSMETA,                          // K4c chunk x tile offsets, view / chunk table
-  S_K6ORDER,                                // K6 launch order (largest tiles first)
-  S_K6PART,                                 // K6 sub-tile block partial sums (variants 9-11)
+  S_K6PART,                                 // K6 strip partial sums (four 16x4 strips per tile)
   S_OPTIM,                                  // NEXT-3 loss partial sums
   S_NSLOTS
 };
@@ -164,17 +163,11 @@ struct gsr_ctx {
   double bytes[GSR_N_STAGES] = {};
   int64_t launches[GSR_N_STAGES] = {};
   int64_t last_nvis = 0, last_keys = 0;  // of the last gsr_bin_sort (byte accounting)
-  int sort_variant = 1;       // sort pass: 1 onesweep (default), 2 persistent onesweep, 3 reduce-then-scan (GSR_SORT)
-  int sort_kpt32 = 12;        // tile-sort keys per thread (GSR_KPT: 8 or 12)
-  int composite_stages = 4;   // K6 ring depth (GSR_STAGES: 4 or 8)
-  int composite_pix = 1;      // K6 pixels per consumer lane (GSR_PIX: 1 or 2)
   bool depth_keys64 = false;  // force the 64-bit depth-sort keys (GSR_DKEY64=1)
   int bw_warps = 2;           // K6b warps per block: 2 (sub-tile blocks) or 8 (GSR_BWNW)
   int bw_reduce = 2;          // K6b warp reduction: 0 shuffle trees, 1 smem atomics, 2 butterfly (GSR_BWRED)
-  bool k6_order = false;      // K6 largest-tile-first launch order (GSR_K6ORDER=1)
   int pack_tile_keys = 1;     // K3 -> K4c keys as one (tile << gbits | g) word when they fit (GSR_PACK=0: two planes)
   int tile_sort_mode = 0;     // 0 / 1: K4c counting scatter up to 12,288 tiles per view, 2: K4b radix (GSR_TSORT=radix)
-  int composite_variant = 10; // K6: 1 block-sync LDG, 2 TMA bulk/record, 3 TMA gather4, 4 cp.async, 5 warp-independent LDG, 6 = 5 + exact ellipse-box cull, 7 = 6 with per-warp TMA gather4 buffers (GSR_STAGES: 2 or 4), 8 = 6 with compacted hit staging + counted hit loop, 9 / 10 / 11 = 8 in blocks of 4 / 2 / 1 warps on part of a tile (10 default)
 };
 
 namespace gsr {
