@@ -787,17 +787,28 @@ __device__ __forceinline__ void cs_locate(const uint32_t* __restrict__ meta, int
   k1 = min(k0 + ch, vs[v + 1]);
 }
 
-__global__ void __launch_bounds__(256) cs_meta(const uint2* __restrict__ ranges, int V, uint32_t tpv, uint32_t K,
-                                               uint32_t* __restrict__ meta, uint32_t ch) {
-  if (threadIdx.x != 0) return;
-  uint32_t pb = 0;
-  for (int v = 0; v <= V; ++v) {
-    const uint32_t s = v < V ? ranges[(size_t)v * tpv].x : K;
+__global__ void __launch_bounds__(64) cs_meta(const uint2* __restrict__ ranges, int V, uint32_t tpv, uint32_t K,
+                                              uint32_t* __restrict__ meta, uint32_t ch) {
+  // one thread per view (V <= 64): first key, chunk count, then an exclusive
+  // scan of the chunk counts over two warps
+  __shared__ uint32_t s_w[2];
+  const int v = threadIdx.x, lane = v & 31, warp = v >> 5;
+  uint32_t s = K, c = 0;
+  if (v < V) {
+    s = ranges[(size_t)v * tpv].x;
+    const uint32_t e = (v + 1 < V) ? ranges[(size_t)(v + 1) * tpv].x : K;
+    c = (e - s + ch - 1) / ch;
+  }
+  const uint32_t inc = warp_incl_scan<uint32_t>(c);
+  if (lane == 31) s_w[warp] = inc;
+  __syncthreads();
+  const uint32_t pb = inc - c + (warp ? s_w[0] : 0u);
+  if (v < V) {
     meta[v] = s;
     meta[(V + 1) + v] = pb;
-    if (v < V) {
-      const uint32_t e = (v + 1 < V) ? ranges[(size_t)(v + 1) * tpv].x : K;
-      pb += (e - s + ch - 1) / ch;
+    if (v == V - 1) {
+      meta[V] = K;
+      meta[(V + 1) + V] = pb + c;  // the total chunk count
     }
   }
 }
@@ -1447,7 +1458,7 @@ static gsr_status bin_sort_impl(gsr_ctx* ctx, const uint32_t* bin_rec, int64_t n
     const uint32_t tslice = (uint32_t)((tpv + nslice - 1) / nslice);
     const size_t smem = (size_t)((tslice + 7) & ~7u) * (8 + 2 * 8);
     sp = stage_begin(ctx, GSR_STAGE_TILE_SORT, st);
-    cs_meta<<<1, 32, 0, st>>>((const uint2*)ranges, n_views, (uint32_t)tpv, (uint32_t)K, (uint32_t*)meta, ch);
+    cs_meta<<<1, 64, 0, st>>>((const uint2*)ranges, n_views, (uint32_t)tpv, (uint32_t)K, (uint32_t*)meta, ch);
     cs_hist<<<(unsigned)nchunks_max, 256, tpv * 4, st>>>((const uint32_t*)tka, (const uint32_t*)meta, n_views,
                                                           (uint32_t)tpv, (uint32_t*)hm, gbits, ch);
     cs_scan<<<(unsigned)((T + 255) / 256), 256, 0, st>>>((const uint2*)ranges, (const uint32_t*)meta, n_views,
