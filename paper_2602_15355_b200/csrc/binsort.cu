@@ -289,7 +289,7 @@ __global__ void __launch_bounds__(256) hist_u64(const uint64_t* __restrict__ key
 //           vals_out and, if keys64 != null, the full 64-bit key
 //           (key << 32) | depth_plane[view * nper + g].
 #ifndef OS_MINB12
-#define OS_MINB12 4  // 12-key tiles: 4 blocks per SM (64 registers, small spills) measured +0.4 % over 3
+#define OS_MINB12 4  // 4 blocks per SM (64 registers, small spills): 12-key tiles +0.4 % over 3 (round 1); 16-key tiles 4 vs 3 blocks -1 % depth-sort time (round 2)
 #endif
 template <typename KeyT, int KPT, int MODE>
 __global__ void __launch_bounds__(256, (KPT <= 8 ? 4 : OS_MINB12)) onesweep(const KeyT* __restrict__ kin, const uint32_t* __restrict__ vin,
@@ -1138,7 +1138,7 @@ int bits_for(uint64_t count) {  // ceil(log2(count)), 0 for count <= 1
 }
 
 constexpr int KPT64 = 12;  // onesweep u64 keys: 3072 keys per block
-constexpr int KPT32 = 12;  // onesweep u32 keys: 3072 keys per block
+constexpr int KPT32 = 16;  // onesweep u32 keys: 4096 keys per block (round 2: 16 keys 3,172 vs 12 keys 3,159 views/s on the bench; 20 keys slower)
 
 template <typename KeyT>
 constexpr size_t pass_tile() {
