@@ -763,7 +763,7 @@ __global__ void __launch_bounds__(1024) k5_ranges(const uint32_t* __restrict__ c
 // DRAM traffic per key: 4 B (hist) + 4 B (packed) or 8 B read + 4 B write
 // (scatter) + the H matrix (CS_CHUNK = 64 K keys: ~0.15 B/key at c3), vs
 // 28 B/key for two radix passes.
-constexpr int CS_KPT = 8;
+constexpr int CS_KPT = 16;  // keys per lane per sub-round (round 2: 16 3,190 / 12 3,186 / 8 3,173 / 6 3,156 views/s)
 #ifndef CS_CHUNK_KEYS
 #define CS_CHUNK_KEYS 65536  // measured: 64 K 2,895, 32 K 2,887, 16 K 2,880 views/s
 #endif
