@@ -472,10 +472,23 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
 
+    def count_step():
+        """The fragment counters of one step (untimed; they depend only on the
+        workload, which every step repeats): the timed steps run K6 without
+        the counting bookkeeping."""
+        scorer.count_fragments = True
+        scorer.reset_counters()
+        step()
+        barrier()
+        fr = scorer.n_frag.clone().to(torch.float64)
+        scorer.count_fragments = False
+        if world > 1:
+            dist.all_reduce(fr, op=dist.ReduceOp.SUM)
+        return fr.tolist()
+
     def timed(k, e2e=False, stage_timing=False):
         scorer.timing(stage_timing)
         scorer.timing_read()
-        scorer.reset_counters()
         barrier()
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         t0 = time.perf_counter()
@@ -489,12 +502,11 @@ def main():
         stages = scorer.timing_read()
         scorer.timing(False)
         t = torch.tensor([ms, wall * 1e3], dtype=torch.float64, device=dev)
-        fr = scorer.n_frag.clone().to(torch.float64)
         if world > 1:
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            dist.all_reduce(fr, op=dist.ReduceOp.SUM)
-        return float(t[0].item()), float(t[1].item()), fr.tolist(), stages
+        return float(t[0].item()), float(t[1].item()), [c * k for c in counts], stages
 
+    counts = count_step()
     for _ in range(args.warmup):
         step()
     barrier()
@@ -564,15 +576,17 @@ def main():
     iso = iso_sort = iso_stages = with_maps = None
     if not args.no_extras and world == 1:
         iso_scorer = ViewScorer(G, batch_views=args.batch_views, n_slots=1)
-        iso_scorer.score_views(cams)
+        iso_scorer.reset_counters()
+        iso_scorer.score_views(cams)  # counted, untimed
+        torch.cuda.synchronize()
+        ifr = iso_scorer.n_frag.to(torch.float64).tolist()
+        iso_scorer.count_fragments = False
         iso_scorer.timing(True)
         iso_scorer.timing_read()
-        iso_scorer.reset_counters()
         torch.cuda.synchronize()
         iso_scorer.score_views(cams)
         torch.cuda.synchronize()
         ist = iso_scorer.timing_read()
-        ifr = iso_scorer.n_frag.to(torch.float64).tolist()
         it = ist["composite"]["ms"] / 1e3
         iso_ops = (28.0 * ifr[1] + 8.0 * ifr[0]) / it / 1e12
         iso = {"bound": "alu", "kernel": "k6_composite (one stream)", "achieved": round(iso_ops, 2),

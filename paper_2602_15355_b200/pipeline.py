@@ -98,6 +98,9 @@ class ViewScorer:
             else:
                 self.slots.append(_Slot(self.dev, self.V, field.n, torch.cuda.Stream(self.dev)))
         self.ctx = self.slots[0].ctx
+        # diagnostic fragment counters (n_frag: blended fragments, evaluated
+        # pairs); off, K6 runs its variant without the per-hit bookkeeping
+        self.count_fragments = True
         self.last_keys: List[int] = []
         self.order_cache = None
         if order_tiles is not None:
@@ -211,7 +214,8 @@ class ViewScorer:
             self._ensure_gray(S, V, H, W, V * tiles_per_view(cams[0]))
             gray = S.gray
         gsr.gsr_composite(S.ctx, S.rec, n, S.vals, S.ranges, cams, S.partial, rgbu=images, t_final=t_final,
-                          n_contrib=n_contrib, n_frag=S.n_frag, gray=gray, stream=cs)
+                          n_contrib=n_contrib,
+                          n_frag=S.n_frag if self.count_fragments else None, gray=gray, stream=cs)
         gsr.gsr_score_views(S.ctx, S.partial, cams, scores_out, cs)
         if sobel_out is not None:
             gsr.gsr_sobel_scores(S.ctx, gray, cams, S.partial2, sobel_out, cs)

@@ -29,6 +29,7 @@ def child(views: int, slots: int):
     G = Gaussians(torch.from_numpy(sc.field.planes).cuda(), sc.field.sh_degree)
     cams = sc.cameras[:: max(1, len(sc.cameras) // views)][:views]
     s = ViewScorer(G, batch_views=32, n_slots=slots)
+    s.count_fragments = False  # as bench.py times it
     s.score_views(cams)
     torch.cuda.synchronize()
     s.timing(True)
