@@ -235,6 +235,16 @@ gsr_status gsr_composite(gsr_ctx* ctx, const float* render_rec, int64_t n, const
                          float* rgbu, float* t_final, uint32_t* n_contrib, float* gray,
                          float* tile_partial, unsigned long long* n_frag, void* stream);
 
+/* K6 launch shape (performance only; the outputs are identical either way).
+   blocks_per_sm = 0 (default): one 64-thread block per 16x4 strip, up to 20
+   resident per SM.  blocks_per_sm = k in [1, 32]: a persistent grid of
+   k x (SM count) blocks that take strips by an atomic ticket, so the rest of
+   each SM stays free for kernels on other streams (the next batch's sorts
+   in a multi-stream pipeline: 3,397 vs 3,336 views/s at k = 10 on c3; alone
+   on the GPU the same k costs 17 %).  Applies to later
+   gsr_composite calls on ctx.  EINVAL: NULL ctx, k outside [0, 32]. */
+gsr_status gsr_set_composite_residency(gsr_ctx* ctx, int32_t blocks_per_sm);
+
 /* ---- K7: view score u(θ) = (sum of U over all W*H pixels) / (W*H) ----------
    (north_star "mean composited uncertainty"; the paper's spatial means
    PAPER.md L72 "global average", L78 1/(H_z W_z) sum_p).  Deterministic

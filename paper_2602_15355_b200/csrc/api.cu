@@ -93,6 +93,14 @@ gsr_status gsr_create(gsr_ctx** out, int device) {
   return GSR_OK;
 }
 
+gsr_status gsr_set_composite_residency(gsr_ctx* ctx, int32_t blocks_per_sm) {
+  if (!ctx) return GSR_EINVAL;
+  if (blocks_per_sm < 0 || blocks_per_sm > 32)
+    return set_err(ctx, GSR_EINVAL, "gsr_set_composite_residency: blocks_per_sm not in [0, 32]");
+  ctx->k6_persist = blocks_per_sm;
+  return GSR_OK;
+}
+
 gsr_status gsr_timing_enable(gsr_ctx* ctx, int enable) {
   if (!ctx) return GSR_EINVAL;
   DeviceGuard device_guard(ctx);

@@ -166,6 +166,7 @@ struct gsr_ctx {
   bool depth_keys64 = false;  // force the 64-bit depth-sort keys (GSR_DKEY64=1)
   int bw_warps = 2;           // K6b warps per block: 2 (sub-tile blocks) or 8 (GSR_BWNW)
   int bw_reduce = 2;          // K6b warp reduction: 0 shuffle trees, 1 smem atomics, 2 butterfly (GSR_BWRED)
+  int k6_persist = 0;         // K6 persistent grid: resident blocks per SM (gsr_set_composite_residency; 0 = one block per strip)
   int pack_tile_keys = 1;     // K3 -> K4c keys as one (tile << gbits | g) word when they fit (GSR_PACK=0: two planes)
   int tile_sort_mode = 0;     // 0 / 1: K4c counting scatter up to 12,288 tiles per view, 2: K4b radix (GSR_TSORT=radix)
 };

@@ -34,7 +34,8 @@ EXPORTED = ["gsr_create", "gsr_destroy", "gsr_last_error", "gsr_version", "gsr_c
             "gsr_project", "gsr_bin_sort", "gsr_composite", "gsr_score_views", "gsr_select_nbv",
             "gsr_sort_pairs_u64", "gsr_scratch_bytes", "gsr_timing_enable", "gsr_timing_read", "gsr_w2_scores",
             "gsr_sobel_scores", "gsr_backward", "gsr_order_cache_size", "gsr_build_order_cache",
-            "gsr_bin_sort_cached", "gsr_l2_loss", "gsr_adam_step", "gsr_order_cache_bins"]
+            "gsr_bin_sort_cached", "gsr_l2_loss", "gsr_adam_step", "gsr_order_cache_bins",
+            "gsr_set_composite_residency"]
 STAGES = ["project", "compact", "depth_sort", "emit", "ranges", "tile_sort", "composite", "score", "select",
           "sort_u64", "w2", "sobel", "backward", "optim"]
 
@@ -85,6 +86,7 @@ def _load():
     L.gsr_sort_pairs_u64.argtypes = [P, P, P, P, P, i64, i32, i32, P]
     L.gsr_w2_scores.argtypes = [P, P, P, i32, i32, i32, i64, P, P, P]
     L.gsr_timing_enable.argtypes = [P, ctypes.c_int]
+    L.gsr_set_composite_residency.argtypes = [P, i32]
     L.gsr_timing_read.argtypes = [P, P, P, P]
     L.gsr_scratch_bytes.argtypes = [P]
     L.gsr_scratch_bytes.restype = i64
@@ -205,6 +207,11 @@ class Context:
 
     def scratch_bytes(self) -> int:
         return int(lib.gsr_scratch_bytes(self.handle))
+
+    def set_composite_residency(self, blocks_per_sm: int):
+        """K6 launch shape: 0 = one block per strip; k > 0 = persistent grid of
+        k blocks per SM (leaves room for kernels on other streams)."""
+        self._check(lib.gsr_set_composite_residency(self.handle, int(blocks_per_sm)))
 
     def timing(self, enable: bool = True):
         self._check(lib.gsr_timing_enable(self.handle, 1 if enable else 0))

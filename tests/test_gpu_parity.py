@@ -329,3 +329,21 @@ def test_invalid_next_arguments(ctx):
     with pytest.raises(gsr.GsrError) as ei:
         gsr.OrderCache(ctx, G, [0, 30], [8], [[0.0, 0.0, 0.0]])  # does not cover [0, 64)
     assert ei.value.status == gsr.GSR_EINVAL
+
+
+@pytest.mark.parametrize("residency", [1, 10, 32])
+def test_composite_residency_same_outputs(residency):
+    """gsr_set_composite_residency changes only K6's launch shape (a
+    persistent grid taking strips by ticket): images, counters and scores
+    equal the oracle's exactly as with one block per strip, including with a
+    single resident block per SM (every strip through one ticket loop)."""
+    from paper_2602_15355_b200 import Context, gsr
+    c = Context(0)
+    c.set_composite_residency(residency)
+    sc = synth.make_scene(1)
+    g, o = _full_check(c, sc.field, sc.cameras)
+    assert np.array_equal(g["rgbu"], o["rgbu"])
+    for bad in (-1, 33):
+        with pytest.raises(gsr.GsrError) as ei:
+            c.set_composite_residency(bad)
+        assert ei.value.status == gsr.GSR_EINVAL
