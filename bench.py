@@ -379,18 +379,21 @@ def bench_configs(dev, steps: int = 3):
         G = Gaussians(torch.from_numpy(sc.field.planes).to(dev), sc.field.sh_degree)
         s = ViewScorer(G, batch_views=16, n_slots=2)
         nv = len(sc.cameras)
-        for _ in range(2):
-            s.score_views(sc.cameras)
+        s.count_fragments = True  # one counted pass, untimed
+        s.reset_counters()
+        s.score_views(sc.cameras)
+        torch.cuda.synchronize()
+        fr = float(s.n_frag[0].item())
+        s.count_fragments = False
+        s.score_views(sc.cameras)
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        s.reset_counters()
         e0.record()
         for _ in range(steps):
             s.score_views(sc.cameras)
         e1.record()
         torch.cuda.synchronize()
         t = e0.elapsed_time(e1) / steps / 1e3
-        fr = float(s.n_frag[0].item()) / steps
         out[synth.CONFIG_NAMES[cfg]] = {"views_per_sec": round(nv / t, 1), "ms_per_pass": round(t * 1e3, 2),
                                         "fragments_per_sec": round(fr / t, 1),
                                         "keys_per_view": int(sum(s.last_keys) / nv)}
@@ -449,7 +452,10 @@ def main():
     planes = torch.empty((P, n, 4), dtype=torch.float32, device=dev)
     planes.copy_(host_planes, non_blocking=False)
     G = Gaussians(planes, 3)
-    scorer = ViewScorer(G, batch_views=args.batch_views, n_slots=args.slots)
+    # K6 as a persistent grid of 10 blocks per SM beside the next batch's sorts
+    # when batches overlap (c3 3,401 vs 3,336 views/s)
+    scorer = ViewScorer(G, batch_views=args.batch_views, n_slots=args.slots,
+                        composite_residency=10 if args.slots > 1 else 0)
 
     def score_fn(c):
         return scorer.score_views(c)
@@ -559,10 +565,19 @@ def main():
             "work": "28 FP32 ops per (pixel, list entry) pair the plain definition evaluates + 8 per blended "
                     f"fragment, per launch = {args.batch_views} views",
             "peak_source": f"148 SMs x 128 FP32 lanes x {f_clk / 1e6:.0f} MHz (median SM clock under load)",
+            "note": "SURVEY.md §8 L292-306 work model: the culled kernel skips most of the plain definition's "
+                    "pairs and runs its hit loop in packed FP32, so this throughput of plain-definition work can "
+                    "exceed the lane peak alone on the GPU (roofline_isolated); pipe utilisation is ncu.fma_pipe_pct. "
+                    "In the pipeline K6 runs as a persistent grid of 10 blocks per SM beside the next batch's sort "
+                    "kernels, so its launch spans include SM time the sorts use",
             # its event spans / the device step time (stage spans of the two
             # slots overlap, so they do not add up to the step)
             "share_of_step": round(st_ms["composite"] / (ms / args.steps), 3),
             "launches_per_step": n_comp}
+    if traffic.get("k6_ncu", {}).get("warp_inst") and frags[1] > 0:
+        # lane-instructions K6 issues per evaluated (pixel, entry) pair
+        roof["lane_inst_per_eval_pair"] = round(
+            traffic["k6_ncu"]["warp_inst"] * 32 / (frags[1] / max(1, n_comp // 2 * args.steps)), 2)
     ach_sort = st_by["tile_sort"] / (st_ms["tile_sort"] / 1e3) / 1e9
     roof_sort = {"bound": "hbm", "kernel": "tile_sort (K4c counting scatter: chunk histograms + column scan + "
                                             "ranked scatter)", "achieved": round(ach_sort, 1),
@@ -577,6 +592,7 @@ def main():
     if not args.no_extras and world == 1:
         iso_scorer = ViewScorer(G, batch_views=args.batch_views, n_slots=1)
         iso_scorer.reset_counters()
+        iso_scorer.count_fragments = True
         iso_scorer.score_views(cams)  # counted, untimed
         torch.cuda.synchronize()
         ifr = iso_scorer.n_frag.to(torch.float64).tolist()

@@ -34,9 +34,6 @@ def cache_bins(field: Gaussians, tile_start, tau: float = CACHE_TAU, ctx: Option
     return gsr.gsr_order_cache_bins(ctx, field, tile_start, tau, CACHE_BASE_BINS, CACHE_HOT_BINS)
 
 
-COMPOSITE_RESIDENCY = 10  # K6 blocks per SM when batches overlap
-
-
 def tiles_per_view(cam) -> int:
     W, H = int(cam["width"]), int(cam["height"])
     return ((W + 15) // 16) * ((H + 15) // 16)
@@ -81,7 +78,7 @@ class ViewScorer:
     the required size; grow by 25 % and retry)."""
 
     def __init__(self, field: Gaussians, batch_views: int = 32, n_slots: int = 3, lod: Optional[gsr.Lod] = None,
-                 order_tiles=None):
+                 order_tiles=None, composite_residency: Optional[int] = None):
         self.field = field
         self.lod = lod  # NEXT-2 LOD blending (opacity multiplier in K1), or None
         # NEXT-2b: (tile_start, bins, centres) -> cached view-direction orderings
@@ -98,16 +95,21 @@ class ViewScorer:
                 ps, pc = {"sort": (hi, lo), "equal": (lo, lo)}.get(os.environ.get("GSR_PRIO", ""), (lo, hi))
                 self.slots.append(_Slot(self.dev, self.V, field.n, torch.cuda.Stream(self.dev, priority=ps),
                                         torch.cuda.Stream(self.dev, priority=pc)))
-                # K6 as a persistent grid of 10 blocks per SM: the next batch's sort
-                # kernels co-run on the SMs' remaining room (3,397 vs 3,336 views/s;
-                # 8 / 12 / 16 / 20: 3,379 / 3,383 / 3,386 / 3,352)
-                self.slots[-1].ctx.set_composite_residency(COMPOSITE_RESIDENCY)
             else:
                 self.slots.append(_Slot(self.dev, self.V, field.n, torch.cuda.Stream(self.dev)))
         self.ctx = self.slots[0].ctx
+        # K6 launch shape (gsr_set_composite_residency): 0 = one block per
+        # strip; k > 0 = a persistent grid of k blocks per SM, so the next
+        # batch's sort kernels co-run on the SMs' remaining room.  Workload-
+        # dependent: c3 3,401 vs 3,336 views/s at k = 10 with
+        # three slots, c2 10,014 vs 10,731 with two, c4 equal
+        self.composite_residency = int(composite_residency or 0)
+        for s_ in self.slots:
+            s_.ctx.set_composite_residency(self.composite_residency)
         # diagnostic fragment counters (n_frag: blended fragments, evaluated
-        # pairs); off, K6 runs its variant without the per-hit bookkeeping
-        self.count_fragments = True
+        # pairs), off by default: K6 then runs its variant without the per-hit
+        # bookkeeping (c2: 3.5 % of the pass)
+        self.count_fragments = False
         self.last_keys: List[int] = []
         self.order_cache = None
         if order_tiles is not None:
@@ -117,7 +119,8 @@ class ViewScorer:
     # ------------------------------------------------------------------ helpers
     @property
     def n_frag(self) -> torch.Tensor:
-        """[blended fragments, evaluated pairs] summed over slots (device)."""
+        """[blended fragments, evaluated pairs] summed over slots (device),
+        accumulated by passes run with ``count_fragments = True``."""
         return torch.stack([s.n_frag for s in self.slots]).sum(0)
 
     def reset_counters(self):
