@@ -306,6 +306,27 @@ def bench_backward(G, dev, reps: int = 3):
             fw += e[0].elapsed_time(e[1])
             bw += e[1].elapsed_time(e[2])
     fw, bw = fw / reps, bw / reps
+    # K6b / K1b device times (their own stages) and K6b's FP32 roofline: the
+    # walk's evaluated pairs E and blended fragments F from one counted,
+    # untimed composite of the same batch; work = 28 E (the forward's walk) +
+    # 56 F (per blended pair: the forward blend 8, 1 / (1 - alpha) 2, dL/dalpha
+    # over four channels 24, dL/dpower and the ten parameter gradients 22)
+    from paper_2602_15355_b200 import gsr
+    nf = torch.zeros(2, dtype=torch.int64, device=dev)
+    gsr.gsr_composite(r.ctx, r.rec, G.n, r.vals, r.ranges, cams, r.partial, n_frag=nf)
+    torch.cuda.synchronize()
+    E, F = float(nf[1].item()), float(nf[0].item())
+    r.ctx.timing(True)
+    r.ctx.timing_read()
+    for _ in range(reps):
+        r.backward(2.0 * (img - target), grads)
+    st = r.ctx.timing_read()
+    r.ctx.timing(False)
+    k6b_ms, k1b_ms = st["backward"]["ms"] / reps, st["backward_project"]["ms"] / reps
+    peak_ops = 148 * 128 * 1965e6 / 1e12
+    k6b_ops = (28.0 * E + 56.0 * F) / (k6b_ms / 1e3) / 1e12
+    k1b_gbs = st["backward_project"]["bytes"] / reps / (k1b_ms / 1e3) / 1e9
+    peaks = load_peaks()
     # one UPDATE_GS refinement iteration (render, L2 loss gradient, backward,
     # projected Adam) on a copy of the field against the perturbed captures
     from paper_2602_15355_b200 import Gaussians
@@ -326,6 +347,16 @@ def bench_backward(G, dev, reps: int = 3):
     return {"metric": "forward_backward_views_per_sec", "value": round(16 / ((fw + bw) / 1e3), 1), "unit": "views/s",
             "forward_ms_per_batch": round(fw, 3), "backward_ms_per_batch": round(bw, 3),
             "refine_iterations_per_sec": round(1e3 / it, 1), "refine_ms_per_iteration": round(it, 3),
+            "k6b_ms_per_batch": round(k6b_ms, 3), "k1b_ms_per_batch": round(k1b_ms, 3),
+            "roofline": {"bound": "alu", "kernel": "k6_backward", "achieved": round(k6b_ops, 2),
+                         "peak": round(peak_ops, 2), "unit": "Top/s", "frac": round(k6b_ops / peak_ops, 4),
+                         "work": "28 FP32 ops per evaluated (pixel, entry) pair of the forward walk + 56 per "
+                                 "blended fragment (gradient chain), per 16-view batch",
+                         "peak_source": "148 SMs x 128 FP32 lanes x 1965 MHz (max SM clock)"},
+            "roofline_k1b": {"bound": "hbm", "kernel": "k1_backward", "achieved": round(k1b_gbs, 1),
+                             "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": round(k1b_gbs / peaks["hbm_gbs"], 4),
+                             "work": "40 B per visible pair + 4 B per (view, g) + 2 x 16 B per plane per Gaussian "
+                                     "(ALU-heavy: the chain rule per (view, g) at SH degree 3)"},
             "config": "c3 field (1M Gaussians, SH 3), 16 views 800x800, L2 loss vs a perturbed image; "
                       "refinement iteration = forward + loss gradient + backward + Adam on 16 views"}
 

@@ -353,9 +353,10 @@ enum {
   GSR_STAGE_SORT_U64 = 9,   /* utility sort (histogram + passes) */
   GSR_STAGE_W2 = 10,        /* NEXT-1 latent W2 scorer */
   GSR_STAGE_SOBEL = 11,     /* NEXT-4 Sobel image term */
-  GSR_STAGE_BACKWARD = 12,  /* NEXT-3 backward rasterizer (K6b + K1b) */
+  GSR_STAGE_BACKWARD = 12,  /* NEXT-3 backward rasterizer K6b (+ the grad2d clear) */
   GSR_STAGE_OPTIM = 13,     /* NEXT-3 loss gradient + Adam step */
-  GSR_N_STAGES = 14
+  GSR_STAGE_BACKWARD_PROJECT = 14, /* NEXT-3 K1b: chain rule to the field parameters */
+  GSR_N_STAGES = 15
 };
 /* enable != 0: bracket every stage with CUDA events on its launch stream. */
 gsr_status gsr_timing_enable(gsr_ctx* ctx, int enable);

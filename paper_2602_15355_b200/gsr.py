@@ -37,7 +37,7 @@ EXPORTED = ["gsr_create", "gsr_destroy", "gsr_last_error", "gsr_version", "gsr_c
             "gsr_bin_sort_cached", "gsr_l2_loss", "gsr_adam_step", "gsr_order_cache_bins",
             "gsr_set_composite_residency"]
 STAGES = ["project", "compact", "depth_sort", "emit", "ranges", "tile_sort", "composite", "score", "select",
-          "sort_u64", "w2", "sobel", "backward", "optim"]
+          "sort_u64", "w2", "sobel", "backward", "optim", "backward_project"]
 
 
 class GsrError(RuntimeError):
