@@ -94,6 +94,44 @@ __device__ __forceinline__ float exp_spec_core_fast(float x, float c7) {  // x i
   return p * __int_as_float((int)((__float_as_uint(t) << 23) + 0x3f800000u));
 }
 
+// Packed FP32 (sm_100a FADD2 / FMUL2 / FFMA2): two IEEE round-to-nearest
+// results per instruction, each identical to the scalar operation.  ptxas
+// contracts a packed mul feeding a packed add into FFMA2 even under
+// -fmad=false (and -Xptxas --fmad=false), so no packed product here ever
+// feeds a packed add / sub.
+typedef unsigned long long f32x2;
+__device__ __forceinline__ f32x2 pk2(float lo, float hi) {
+  f32x2 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ f32x2 bc2(float v) { return pk2(v, v); }
+__device__ __forceinline__ float lo2(f32x2 v) {
+  float a;
+  asm("mov.b64 {%0, _}, %1;" : "=f"(a) : "l"(v));
+  return a;
+}
+__device__ __forceinline__ float hi2(f32x2 v) {
+  float b;
+  asm("mov.b64 {_, %0}, %1;" : "=f"(b) : "l"(v));
+  return b;
+}
+__device__ __forceinline__ f32x2 fsub2(f32x2 a, f32x2 b) {
+  f32x2 r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ f32x2 fmul2(f32x2 a, f32x2 b) {
+  f32x2 r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ f32x2 ffma2(f32x2 a, f32x2 b, f32x2 c) {
+  f32x2 r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+
 // ---- tile spans (O1 steps 14-15) ----
 // A Gaussian is listed in tile (tx, ty) iff the tile holds a pixel centre
 // inside the x-extent, over the tile's pixel rows, of the ellipse q <= 11.1
