@@ -347,3 +347,24 @@ def test_composite_residency_same_outputs(residency):
         with pytest.raises(gsr.GsrError) as ei:
             c.set_composite_residency(bad)
         assert ei.value.status == gsr.GSR_EINVAL
+
+
+def test_scorer_fragment_counters_switch():
+    """ViewScorer.count_fragments selects K6's counting variant: on, the
+    counters equal the oracle's (blended fragments, evaluated pairs); off,
+    they stay zero; the scores are identical either way (the counting
+    bookkeeping does not touch the composited values)."""
+    from paper_2602_15355_b200 import Gaussians
+    from paper_2602_15355_b200.pipeline import ViewScorer
+    sc = synth.make_scene(1)
+    G = Gaussians(torch.from_numpy(sc.field.planes).cuda(), sc.field.sh_degree)
+    o = oracle_batch(sc.field, sc.cameras)
+    s = ViewScorer(G, batch_views=16, n_slots=2)
+    s.reset_counters()
+    off = s.score_views(sc.cameras).cpu().numpy()
+    assert s.n_frag.cpu().tolist() == [0, 0]
+    s.count_fragments = True
+    on = s.score_views(sc.cameras).cpu().numpy()
+    assert s.n_frag.cpu().tolist() == [o["n_frag"], o["n_eval"]]
+    assert np.array_equal(on, off)
+    np.testing.assert_allclose(on, o["scores"], rtol=SCORE_RTOL, atol=0)
