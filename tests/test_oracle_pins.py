@@ -416,6 +416,24 @@ def test_termination_stops_before_blending():
     np.testing.assert_allclose(out["rgbu"][8, 8], [0.99, 0, 0, 0.99], rtol=1e-7)
 
 
+def test_termination_threshold_closed_form():
+    """The 1e-4 stop threshold itself (O5): a stack of eight identical layers
+    centred on a pixel, each alpha = 0.8 there (exp(0) = 1 exactly, o = 0.8),
+    blends exactly k = floor(ln 1e-4 / ln 0.2) = 5 layers (0.2^5 = 3.2e-4 >=
+    1e-4 > 0.2^6 = 6.4e-5, both far from the threshold), T_final = 0.2^5,
+    U = 1 - 0.2^5.  A threshold of 1e-3 would stop after 4, of 1e-5 after 7."""
+    k = int(np.floor(np.log(1e-4) / np.log(0.2)))
+    assert k == 5 and 0.2 ** k > 1e-3 / 4 and 0.2 ** (k + 1) < 1e-4
+    cam = axis_camera(17, 17, 50.0, cx=8.5, cy=8.5)
+    n = 8
+    fld = field_from([[0, 0, 1.0 + 0.25 * i] for i in range(n)], [[0.05] * 3] * n, [[1, 0, 0, 0]] * n,
+                     [0.8] * n, [[0, 0, 0]] * n, [1] * n)
+    out = oracle.render_view(fld, cam)
+    assert out["n_contrib"][8, 8] == k
+    np.testing.assert_allclose(out["t_final"][8, 8], 0.2 ** k, rtol=1e-5)
+    np.testing.assert_allclose(out["rgbu"][8, 8, 3], 1.0 - 0.2 ** k, rtol=1e-5)
+
+
 @pytest.mark.parametrize("seed,deg", [(0, 0), (1, 1), (2, 2), (3, 3), (4, 3)])
 def test_brute_force_equals_tiled_bit_exact(seed, deg):
     """Tiled (per-tile sorted lists) == brute force (all Gaussians, global depth
