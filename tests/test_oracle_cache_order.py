@@ -52,6 +52,27 @@ def test_cached_equals_exact_when_looking_along_a_bin():
     assert a["order"][0] == np.argmin(fld.planes[0, :, 0]) and np.array_equal(a["rgbu"], b["rgbu"])
 
 
+def test_cached_tiles_visited_front_to_back():
+    """Two tiles split at x = 0 (tile 0: x < 0, tile 1: x >= 0) seen along +x
+    from x = -3: tiles visited front to back (tile 0 first) with each tile in
+    its bin-0 order give the global depth order, so the render equals the
+    exact-sort render bit for bit -- the tiles overlap on screen, so visiting
+    them back to front would not."""
+    rng = np.random.default_rng(2)
+    n = 240
+    x = np.sort(rng.uniform(-1, 1, n))
+    means = np.stack([x, rng.uniform(-0.3, 0.3, n), rng.uniform(-0.4, 0.4, n)], 1)
+    fld = field_from(means, np.exp(rng.normal(-2.3, 0.3, (n, 3))), rng.normal(size=(n, 4)),
+                     rng.uniform(0.3, 0.9, n), rng.uniform(0, 1, (n, 3)), rng.uniform(0, 1, n))
+    split = int(np.searchsorted(x, 0.0))
+    start = np.array([0, split, n])
+    centres = np.array([[-0.5, 0.0, 0.0], [0.5, 0.0, 0.0]])
+    cam = synth.look_at([-3.0, 0.0, 0.0], [0.0, 0.0, 0.0], 64, 48, 60.0)
+    a = co.render_view_cached(fld, cam, start, [8, 8], centres)
+    b = oracle.render_view(fld, cam)
+    assert 0 < split < n and np.array_equal(a["rgbu"], b["rgbu"])
+
+
 def test_cached_vs_exact_fidelity_on_flyover():
     """nearest-bin cached order vs exact per-frame depth sort, mean
     per-pixel |RGB| difference <= 0.02 on the default fly-over scene at 8
