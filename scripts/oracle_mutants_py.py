@@ -50,6 +50,17 @@ MUTANTS = [
      "out[k] = s + np.lexsort((np.arange(e - s), key))", "out[k] = s + np.lexsort((np.arange(e - s), -key))"),
     ("oracle/cache_order.py", "tests/test_oracle_cache_order.py", "tile visiting order back to front",
      "order = np.lexsort((np.arange(len(centres)), depth))", "order = np.lexsort((np.arange(len(centres)), -depth))"),
+    # the backward oracle's float64 forward (pinned against the float32 oracle's image)
+    ("oracle/backward.py", "tests/test_oracle_backward.py", "backward forward: j02 sign",
+     "j02, j12 = -(fx * tx) / (vz * vz), -(fy * ty) / (vz * vz)", "j02, j12 = (fx * tx) / (vz * vz), -(fy * ty) / (vz * vz)"),
+    ("oracle/backward.py", "tests/test_oracle_backward.py", "backward forward: no dilation",
+     "a, b, c = Sp[:, 0, 0] + 0.3, Sp[:, 0, 1], Sp[:, 1, 1] + 0.3", "a, b, c = Sp[:, 0, 0], Sp[:, 0, 1], Sp[:, 1, 1]"),
+    ("oracle/backward.py", "tests/test_oracle_backward.py", "backward forward: alpha clamp at 1",
+     "alpha = torch.clamp(o[g] * torch.exp(power), max=0.99)", "alpha = torch.clamp(o[g] * torch.exp(power), max=1.0)"),
+    ("oracle/backward.py", "tests/test_oracle_backward.py", "backward forward: T *= alpha",
+     "Tacc = torch.where(mk, Tacc * (1 - alpha), Tacc)", "Tacc = torch.where(mk, Tacc * alpha, Tacc)"),
+    ("oracle/backward.py", "tests/test_oracle_backward.py", "backward forward: no colour clamp",
+     "rgb = torch.clamp((Y[:, :, None] * P[\"sh\"]).sum(1), min=0.0)", "rgb = (Y[:, :, None] * P[\"sh\"]).sum(1)"),
 ]
 
 

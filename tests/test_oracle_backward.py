@@ -25,6 +25,28 @@ def test_torch_forward_matches_float32_oracle(deg):
     assert np.abs(img - oracle.render_view(fld, cam)["rgbu"]).max() < 2e-6
 
 
+def test_torch_forward_matches_float32_oracle_with_alpha_clamp():
+    """Opaque layers (o = 1) centred on pixel centres reach alpha = 0.99 (the
+    O5 clamp) at those pixels: the float64 forward still reproduces the
+    float32 oracle image there, and dL/do of a clamped pixel is zero (the
+    clamp's derivative)."""
+    cam = axis_camera(17, 17, 50.0, cx=8.5, cy=8.5)
+    fld = field_from([[0, 0, 1.0], [0.02, -0.03, 1.6]], [[0.05] * 3] * 2, [[1, 0, 0, 0]] * 2, [1.0, 1.0],
+                     [[1, 0.5, 0], [0, 0.5, 1]], [0.7, 0.2])
+    off, idx = bw.frozen_lists(fld, cam)
+    P = bw.params_from_field(fld)
+    img = bw.render_t(P, cam, 0, off, idx)
+    ref = oracle.render_view(fld, cam)["rgbu"]
+    assert np.abs(img.detach().numpy() - ref).max() < 2e-6
+    assert abs(float(ref[8, 8, 0]) - 0.99) < 1e-6  # the front layer's alpha is clamped at the centre
+    # upstream gradient only at the clamped centre pixel: the front layer's
+    # opacity gradient there is zero
+    G = torch.zeros(17, 17, 4, dtype=torch.float64)
+    G[8, 8] = 1.0
+    (img * G).sum().backward()
+    assert float(P["opac"].grad[0]) == 0.0
+
+
 @pytest.mark.parametrize("deg", [1, 3])
 def test_autograd_matches_central_differences(deg):
     """dL/dtheta (autograd) vs (L(theta + h) - L(theta - h)) / 2h of the same
