@@ -96,3 +96,21 @@ def test_backward_reduction_variants(ctx, red, monkeypatch):
     G = np.random.default_rng(9).normal(size=(2, 33, 40, 4)).astype(np.float32)
     img, got = gpu_forward_backward(c, fld, cams, G)
     _compare(got, bw.backward_views(fld, cams, G), 2)
+
+
+def test_backward_alpha_clamp(ctx):
+    """Opaque layers (o = 1) reach the alpha = 0.99 clamp at their centres,
+    where K6b's power and opacity gradients must vanish: gradients match the
+    float64 oracle on a scene of such layers."""
+    from tests.helpers import axis_camera, field_from
+    rng = np.random.default_rng(11)
+    n = 12
+    means = np.stack([rng.uniform(-0.2, 0.2, n), rng.uniform(-0.2, 0.2, n), 1.0 + 0.2 * np.arange(n)], 1)
+    means[::3, :2] = 0.0  # every third layer on the axis: its mean projects onto the centre of pixel (16, 14)
+    fld = field_from(means, [[0.06] * 3] * n, [[1, 0, 0, 0]] * n, [1.0] * n, rng.uniform(0, 1, (n, 3)),
+                     rng.uniform(0, 1, n))
+    # cx, cy on a pixel centre: o exp(0) = 1 > 0.99 there, so alpha is clamped
+    cams = np.stack([axis_camera(33, 29, 60.0, cx=16.5, cy=14.5)])
+    G = rng.normal(size=(1, 29, 33, 4)).astype(np.float32)
+    img, got = gpu_forward_backward(ctx, fld, cams, G)
+    _compare(got, bw.backward_views(fld, cams, G), 0)
