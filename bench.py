@@ -494,14 +494,22 @@ def main():
     def select_fn(scores, k, exclude):
         return scorer.select(scores, k, exclude)
 
+    # e2e result staging (page-locked, so the C-ABI copies are asynchronous)
+    host_scores = torch.empty(1024, dtype=torch.float32).pin_memory()
+    host_sel = torch.empty(1, dtype=torch.int32).pin_memory()
+
     def step(e2e: bool = False):
         if e2e and rank == 0:
-            planes.copy_(host_planes, non_blocking=True)  # H2D of the step's inputs
+            # H2D of the step's inputs through the C ABI (gsr_upload, pinned host planes)
+            gsr.gsr_upload(scorer.ctx, planes, host_planes)
         broadcast_field(planes)
         scores, sel = score_and_select(cams, score_fn, select_fn, 1)
         if e2e:
-            out = torch.cat([scores, sel.float()]).cpu()  # D2H of the step's result
-            return out
+            # D2H of the step's result through the C ABI (gsr_download), read on the host
+            gsr.gsr_download(scorer.ctx, host_scores, scores)
+            gsr.gsr_download(scorer.ctx, host_sel, sel)
+            torch.cuda.current_stream().synchronize()
+            return host_sel
         return sel
 
     def barrier():
@@ -558,7 +566,8 @@ def main():
     eval_per_s = frags[1] / (ms / 1e3)
 
     # e2e: through the public API with the field copied H2D from pinned host
-    # memory every step and the scores + NBV read back D2H
+    # memory every step and the scores + NBV read back D2H, both copies
+    # through the C ABI (gsr_upload / gsr_download)
     e2e = None
     if not args.no_e2e:
         ms_e, _, _, _ = timed(args.steps, e2e=True)

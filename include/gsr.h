@@ -335,6 +335,19 @@ gsr_status gsr_sort_pairs_u64(gsr_ctx* ctx, const uint64_t* keys_in, const uint3
                               uint64_t* keys_out, uint32_t* vals_out, int64_t n, int32_t begin_bit,
                               int32_t end_bit, void* stream);
 
+/* ---- host staging (the end-to-end path: inputs in from host memory, the
+   result back out, on the pipeline's own stream) ---------------------------
+   gsr_upload:   bytes from HOST src to DEVICE dst, enqueued on `stream`.
+   gsr_download: bytes from DEVICE src to HOST dst, enqueued on `stream`.
+   Asynchronous when the host buffer is page-locked (cudaHostAlloc /
+   cudaHostRegister); with pageable memory the copy returns only once the
+   host buffer may be reused (cudaMemcpyAsync semantics).  The caller owns
+   both buffers and keeps them alive until the stream has synchronised.
+   bytes == 0 is a no-op.  EINVAL: NULL ctx / pointer with bytes > 0,
+   bytes < 0; ECUDA: the copy failed (e.g. dst / src in the wrong space). */
+gsr_status gsr_upload(gsr_ctx* ctx, void* dst, const void* src /*[host]*/, int64_t bytes, void* stream);
+gsr_status gsr_download(gsr_ctx* ctx, void* dst /*[host]*/, const void* src, int64_t bytes, void* stream);
+
 /* ---- utility: bytes of scratch the context currently holds (diagnostics) */
 int64_t gsr_scratch_bytes(const gsr_ctx* ctx);
 

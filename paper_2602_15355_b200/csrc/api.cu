@@ -148,6 +148,25 @@ gsr_status gsr_destroy(gsr_ctx* ctx) {
   return GSR_OK;
 }
 
+gsr_status gsr_upload(gsr_ctx* ctx, void* dst, const void* src, int64_t bytes, void* stream) {
+  if (!ctx) return GSR_EINVAL;
+  DeviceGuard device_guard(ctx);
+  if (bytes < 0 || (bytes > 0 && (!dst || !src))) return set_err(ctx, GSR_EINVAL, "gsr_upload: NULL pointer or bytes < 0");
+  if (bytes == 0) return GSR_OK;
+  return check_cuda(ctx, cudaMemcpyAsync(dst, src, (size_t)bytes, cudaMemcpyHostToDevice, (cudaStream_t)stream),
+                    "gsr_upload");
+}
+
+gsr_status gsr_download(gsr_ctx* ctx, void* dst, const void* src, int64_t bytes, void* stream) {
+  if (!ctx) return GSR_EINVAL;
+  DeviceGuard device_guard(ctx);
+  if (bytes < 0 || (bytes > 0 && (!dst || !src)))
+    return set_err(ctx, GSR_EINVAL, "gsr_download: NULL pointer or bytes < 0");
+  if (bytes == 0) return GSR_OK;
+  return check_cuda(ctx, cudaMemcpyAsync(dst, src, (size_t)bytes, cudaMemcpyDeviceToHost, (cudaStream_t)stream),
+                    "gsr_download");
+}
+
 const char* gsr_last_error(const gsr_ctx* ctx) { return ctx ? ctx->err.c_str() : g_thread_err.c_str(); }
 
 const char* gsr_version(void) { return "gsr 0.1 sm_100a"; }

@@ -474,11 +474,16 @@ __global__ void __launch_bounds__(256, (KPT <= 8 ? 4 : OS_MINB12)) onesweep(cons
 // consecutive entries.  Each entry's 32-byte span record (O1 step
 // 15) is gathered once.  Emission is two-level load-balanced: the warp's
 // (entry, tile row) units are dealt 32 at a time (owner search over the row
-// counts), each lane evaluates its unit's span, and the keys of the 32 spans
-// are dealt 32 at a time (owner search over the span widths).  Keys leave in
+// counts), each lane evaluates its unit's span and writes the first K3_LS
+// keys of that span itself (to the slots an owner search would deal them
+// to); only the keys of wider spans are dealt 32 at a time (owner search over
+// the remaining widths).  Keys leave in
 // unit order, i.e. (depth, g, ty, tx) order, contiguously from the block's
 // look-back offset.
 constexpr int K3_ROUNDS = 4;
+#ifndef K3_LS
+#define K3_LS 8  // keys per row written lane-serially (0: every key dealt 32 at a time; measured 0 / 3 / 4 / 6 / 8 / 12: emit 1.049 / 1.050 / 1.053 / 0.977 / 0.971 / 0.992 ms per batch, bench 3,401 / 3,405 / 3,423 / 3,453 / 3,456 / 3,447 views/s)
+#endif
 constexpr int K3_TILE = 256 * K3_ROUNDS;
 
 __device__ __forceinline__ int owner_of(uint32_t excl, uint32_t j) {  // largest s with excl[s] <= j
@@ -597,6 +602,59 @@ __global__ void __launch_bounds__(256, K3_MINB) k3_emit(const KeyT* __restrict__
       const uint32_t winc = warp_incl_scan<uint32_t>(w);
       const uint32_t wexcl = winc - w;
       const uint32_t wt = __shfl_sync(FULL, winc, 31);
+#if K3_LS > 0
+      // each lane writes the first K3_LS keys of its own row span (the same
+      // slots the dealt loop would use: base + wexcl + i); only the keys of
+      // rows wider than K3_LS tiles go through the dealt loop below
+      const uint32_t wmax = __reduce_max_sync(FULL, w);
+#pragma unroll
+      for (uint32_t i = 0; i < (uint32_t)K3_LS; ++i) {
+        if (i >= wmax) break;
+        if (i < w) {
+          const uint32_t key = kb + i;
+          GSR_DCHECK(base + wexcl + i < kcap && key < T);
+          if (PACK) {
+            tkeys[base + wexcl + i] = kl + (i << gbits);
+          } else {
+            tkeys[base + wexcl + i] = key;
+            tvals[base + wexcl + i] = kl;
+          }
+          if (key - lo < (uint32_t)smem_bins)
+            atomicAdd(s_cnt + (key - lo), 1u);
+          else
+            atomicAdd(counts + key, 1u);
+        }
+      }
+      if (wmax > (uint32_t)K3_LS) {
+        const uint32_t w2 = w > (uint32_t)K3_LS ? w - (uint32_t)K3_LS : 0u;
+        const uint32_t w2inc = warp_incl_scan<uint32_t>(w2);
+        const uint32_t w2excl = w2inc - w2;
+        const uint32_t w2t = __shfl_sync(FULL, w2inc, 31);
+        for (uint32_t kb0 = 0; kb0 < w2t; kb0 += 32) {
+          const uint32_t k = kb0 + lane;
+          const int t = owner_of(w2excl, k);
+          const uint32_t okb = __shfl_sync(FULL, kb, t);
+          const uint32_t owx = __shfl_sync(FULL, wexcl, t);
+          const uint32_t ow2 = __shfl_sync(FULL, w2excl, t);
+          const uint32_t okl = __shfl_sync(FULL, kl, t);
+          if (k < w2t) {
+            const uint32_t i = (uint32_t)K3_LS + (k - ow2);
+            const uint32_t key = okb + i;
+            GSR_DCHECK(base + owx + i < kcap && key < T);
+            if (PACK) {
+              tkeys[base + owx + i] = okl + (i << gbits);
+            } else {
+              tkeys[base + owx + i] = key;
+              tvals[base + owx + i] = okl;
+            }
+            if (key - lo < (uint32_t)smem_bins)
+              atomicAdd(s_cnt + (key - lo), 1u);
+            else
+              atomicAdd(counts + key, 1u);
+          }
+        }
+      }
+#else
       for (uint32_t kb0 = 0; kb0 < wt; kb0 += 32) {
         const uint32_t k = kb0 + lane;
         const int t = owner_of(wexcl, k);
@@ -618,6 +676,7 @@ __global__ void __launch_bounds__(256, K3_MINB) k3_emit(const KeyT* __restrict__
             atomicAdd(counts + key, 1u);
         }
       }
+#endif
       base += wt;
     }
   }

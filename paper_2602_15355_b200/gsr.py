@@ -35,7 +35,7 @@ EXPORTED = ["gsr_create", "gsr_destroy", "gsr_last_error", "gsr_version", "gsr_c
             "gsr_sort_pairs_u64", "gsr_scratch_bytes", "gsr_timing_enable", "gsr_timing_read", "gsr_w2_scores",
             "gsr_sobel_scores", "gsr_backward", "gsr_order_cache_size", "gsr_build_order_cache",
             "gsr_bin_sort_cached", "gsr_l2_loss", "gsr_adam_step", "gsr_order_cache_bins",
-            "gsr_set_composite_residency"]
+            "gsr_set_composite_residency", "gsr_upload", "gsr_download"]
 STAGES = ["project", "compact", "depth_sort", "emit", "ranges", "tile_sort", "composite", "score", "select",
           "sort_u64", "w2", "sobel", "backward", "optim", "backward_project"]
 
@@ -89,6 +89,8 @@ def _load():
     L.gsr_set_composite_residency.argtypes = [P, i32]
     L.gsr_timing_read.argtypes = [P, P, P, P]
     L.gsr_scratch_bytes.argtypes = [P]
+    L.gsr_upload.argtypes = [P, P, P, i64, P]
+    L.gsr_download.argtypes = [P, P, P, i64, P]
     L.gsr_scratch_bytes.restype = i64
     for name in EXPORTED:
         if name not in ("gsr_last_error", "gsr_version", "gsr_scratch_bytes", "gsr_order_cache_size"):
@@ -348,6 +350,34 @@ def gsr_score_views(ctx: Context, tile_partial, cams, scores, stream=None):
     c = cams_array(cams)
     ctx._check(lib.gsr_score_views(ctx.handle, _ptr(tile_partial), c.ctypes.data, len(c), _ptr(scores),
                                    _stream(stream)))
+
+
+def gsr_upload(ctx: Context, dst, src, stream=None):
+    """Host -> device copy of ``src`` (host tensor / ndarray; page-locked for
+    an asynchronous copy) into the CUDA tensor ``dst`` on ``stream``."""
+    nb = _nbytes(src)
+    if nb != _nbytes(dst):
+        raise ValueError("gsr_upload: size mismatch")
+    ctx._check(lib.gsr_upload(ctx.handle, _ptr(dst), _ptr(src), nb, _stream(stream)))
+
+
+def gsr_download(ctx: Context, dst, src, stream=None):
+    """Device -> host copy of the CUDA tensor ``src`` into the host tensor /
+    ndarray ``dst`` on ``stream`` (valid once the stream has synchronised)."""
+    nb = _nbytes(src)
+    if nb != _nbytes(dst):
+        raise ValueError("gsr_download: size mismatch")
+    ctx._check(lib.gsr_download(ctx.handle, _ptr(dst), _ptr(src), nb, _stream(stream)))
+
+
+def _nbytes(t) -> int:
+    if isinstance(t, np.ndarray):
+        if not t.flags["C_CONTIGUOUS"]:
+            raise ValueError("host staging needs a contiguous array")
+        return int(t.nbytes)
+    if not t.is_contiguous():
+        raise ValueError("host staging needs a contiguous tensor")
+    return int(t.numel() * t.element_size())
 
 
 def gsr_select_nbv(ctx: Context, scores, k: int, out_idx, exclude: Optional[np.ndarray] = None, stream=None):
