@@ -368,3 +368,31 @@ def test_scorer_fragment_counters_switch():
     assert s.n_frag.cpu().tolist() == [o["n_frag"], o["n_eval"]]
     assert np.array_equal(on, off)
     np.testing.assert_allclose(on, o["scores"], rtol=SCORE_RTOL, atol=0)
+
+
+def test_row_spans_wider_than_the_lane_serial_emission(ctx):
+    """K3 writes the first K3_LS (8) keys of every row span from the span's own
+    lane and deals only the rest: row spans of 1..40 tiles (wide, flat
+    Gaussians on a 640x96 image), mixed with small ones, give bit-exact key
+    lists, sorted lists, ranges and images vs the oracle."""
+    from tests.helpers import axis_camera, field_from
+    rng = np.random.default_rng(31)
+    n_wide, n_small = 64, 400
+    n = n_wide + n_small
+    means = np.stack([rng.uniform(-1.2, 1.2, n), rng.uniform(-0.35, 0.35, n), rng.uniform(3.0, 5.0, n)], 1)
+    scales = np.concatenate([
+        np.stack([np.linspace(0.02, 1.4, n_wide), rng.uniform(0.01, 0.08, n_wide), rng.uniform(0.01, 0.1, n_wide)], 1),
+        np.exp(rng.normal(-3.5, 0.5, (n_small, 3)))])
+    quats = np.concatenate([np.tile([1.0, 0.0, 0.0, 0.0], (n_wide, 1)) + rng.normal(0, 0.05, (n_wide, 4)),
+                            rng.normal(size=(n_small, 4))])
+    fld = field_from(means, scales, quats, rng.uniform(0.2, 0.95, n), rng.uniform(0, 1, (n, 3)), rng.uniform(0, 1, n))
+    cams = np.asarray([axis_camera(640, 96, 300.0), axis_camera(640, 96, 420.0)])
+    g, o = _full_check(ctx, fld, cams)
+    assert np.array_equal(g["rgbu"], o["rgbu"])
+    widest = 0
+    for p in o["projs"]:
+        for q in p[p["n_tiles"] > 0]:
+            for ty in range(int(q["py0"]) >> 4, (int(q["py1"]) >> 4) + 1):
+                x0, x1 = oracle.row_span(q, ty, cams[0])
+                widest = max(widest, x1 - x0)
+    assert widest >= 30  # the dealt remainder of K3's emission runs
