@@ -45,6 +45,8 @@ def parse():
     p.add_argument("--batch-views", type=int, default=32)  # measured: 64 2,903 / 32 2,889 / 16 2,866 views/s
     p.add_argument("--slots", type=int, default=3,
                    help="concurrent batch pipelines (stream pairs); measured 3: 3,090, 2: 3,076 views/s")
+    p.add_argument("--k6-residency", type=int, default=10,
+                   help="persistent K6 blocks per SM when batches overlap (gsr_set_composite_residency)")
     p.add_argument("--cpu-views", type=int, default=0, help="oracle sample size (0 = auto)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
@@ -486,7 +488,7 @@ def main():
     # K6 as a persistent grid of 10 blocks per SM beside the next batch's sorts
     # when batches overlap (c3 3,401 vs 3,336 views/s)
     scorer = ViewScorer(G, batch_views=args.batch_views, n_slots=args.slots,
-                        composite_residency=10 if args.slots > 1 else 0)
+                        composite_residency=args.k6_residency if args.slots > 1 else 0)
 
     def score_fn(c):
         return scorer.score_views(c)
