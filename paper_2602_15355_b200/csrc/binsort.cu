@@ -109,7 +109,23 @@ __device__ uint64_t warp_lookback(const uint64_t* words, int64_t bid) {
 // Lanes of the warp holding the same 8-bit digit: 8 independent ballots (ALU
 // pipe, fully pipelined) instead of MATCH.ANY, whose latency dominated the
 // ranking loop in the ncu source view.
+#ifndef OS_PTX
+#define OS_PTX 0
+#endif
 __device__ __forceinline__ uint32_t match_digit8(bool valid, uint32_t d) {
+#if OS_PTX
+  uint32_t pv = __ballot_sync(FULL, valid);
+#pragma unroll
+  for (int b = 0; b < 8; ++b) {
+    uint32_t bb, x;
+    asm("{\n\t.reg .pred p;\n\t.reg .b32 t;\n\t"
+        "and.b32 t, %2, %3;\n\tsetp.ne.u32 p, t, 0;\n\t"
+        "vote.sync.ballot.b32 %0, p, 0xffffffff;\n\tselp.b32 %1, 0, 0xffffffff, p;\n\t}"
+        : "=r"(bb), "=r"(x) : "r"(d), "r"(1u << b));
+    pv &= bb ^ x;
+  }
+  return pv;
+#endif
   uint32_t peers = __ballot_sync(FULL, valid);
 #pragma unroll
   for (int b = 0; b < 8; ++b) {
@@ -822,6 +838,9 @@ __global__ void __launch_bounds__(1024) k5_ranges(const uint32_t* __restrict__ c
 // DRAM traffic per key: 4 B (hist) + 4 B (packed) or 8 B read + 4 B write
 // (scatter) + the H matrix (CS_CHUNK = 64 K keys: ~0.15 B/key at c3), vs
 // 28 B/key for two radix passes.
+#ifndef CS_DBT
+#define CS_DBT 1  // compile-time digit widths for the K4c ranks (measured: tile sort 1.236 -> 1.159 ms per batch, bench 3,453 -> 3,495 views/s)
+#endif
 constexpr int CS_KPT = 16;  // keys per lane per sub-round (round 2: 16 3,190 / 12 3,186 / 8 3,173 / 6 3,156 views/s)
 #ifndef CS_CHUNK_KEYS
 #define CS_CHUNK_KEYS 65536  // measured: 64 K 2,895, 32 K 2,887, 16 K 2,880 views/s
@@ -924,7 +943,26 @@ __global__ void __launch_bounds__(256) cs_scan(const uint2* __restrict__ ranges,
   }
 }
 
-template <int W, bool PACK>
+// Lanes of the warp whose DB-bit digit equals this lane's (DB a compile-time
+// width: every bit test takes an immediate mask; per bit one predicate, one
+// ballot, one select and one LOP3).
+template <int DB>
+__device__ __forceinline__ uint32_t match_digits(bool ok, uint32_t d) {
+  uint32_t peers = __ballot_sync(FULL, ok);
+#pragma unroll
+  for (int b = 0; b < DB; ++b) {
+    // p = bit b of d; bb = ballot(p); x = p ? 0 : ~0; lanes agreeing on bit b = bb ^ x
+    uint32_t bb, x;
+    asm("{\n\t.reg .pred p;\n\t.reg .b32 t;\n\t"
+        "and.b32 t, %2, %3;\n\tsetp.ne.u32 p, t, 0;\n\t"
+        "vote.sync.ballot.b32 %0, p, 0xffffffff;\n\tselp.b32 %1, 0, 0xffffffff, p;\n\t}"
+        : "=r"(bb), "=r"(x) : "r"(d), "r"(1u << b));
+    peers &= bb ^ x;
+  }
+  return peers;
+}
+
+template <int W, bool PACK, int DB = 0>
 __global__ void __launch_bounds__(W * 32, 3) cs_scatter(const uint32_t* __restrict__ tkeys,
                                                      const uint32_t* __restrict__ tvals,
                                                      const uint32_t* __restrict__ meta, int V, uint32_t tpv,
@@ -991,11 +1029,16 @@ __global__ void __launch_bounds__(W * 32, 3) cs_scatter(const uint32_t* __restri
 #pragma unroll
     for (int k = 0; k < CS_KPT; ++k) {
       const bool ok = dg[k] < tn;
-      uint32_t peers = __ballot_sync(FULL, ok);
-      for (int b = 0; b < dbits; ++b) {
-        const bool bit = (dg[k] >> b) & 1u;
-        const uint32_t bb = __ballot_sync(FULL, bit);
-        peers &= bit ? bb : ~bb;
+      uint32_t peers;
+      if constexpr (DB > 0) {
+        peers = match_digits<DB>(ok, dg[k]);  // bits >= dbits are 0 in every ok lane
+      } else {
+        peers = __ballot_sync(FULL, ok);
+        for (int b = 0; b < dbits; ++b) {
+          const bool bit = (dg[k] >> b) & 1u;
+          const uint32_t bb = __ballot_sync(FULL, bit);
+          peers &= bit ? bb : ~bb;
+        }
       }
       uint32_t pre = 0;
       if (ok) pre = wh[dg[k]];
@@ -1523,7 +1566,17 @@ static gsr_status bin_sort_impl(gsr_ctx* ctx, const uint32_t* bin_rec, int64_t n
     cs_scan<<<(unsigned)((T + 255) / 256), 256, 0, st>>>((const uint2*)ranges, (const uint32_t*)meta, n_views,
                                                          (uint32_t)tpv, (uint32_t*)hm);
     const int dbits = std::max(1, bits_for(tslice));
+#if CS_DBT
+    // compile-time digit widths (8 / 10 / 12 / 14 bits), else the runtime loop
+    auto scat = gbits ? (dbits <= 8 ? cs_scatter<8, true, 8> : dbits <= 10 ? cs_scatter<8, true, 10>
+                         : dbits <= 12 ? cs_scatter<8, true, 12> : dbits <= 14 ? cs_scatter<8, true, 14>
+                         : cs_scatter<8, true>)
+                      : (dbits <= 8 ? cs_scatter<8, false, 8> : dbits <= 10 ? cs_scatter<8, false, 10>
+                         : dbits <= 12 ? cs_scatter<8, false, 12> : dbits <= 14 ? cs_scatter<8, false, 14>
+                         : cs_scatter<8, false>);
+#else
     auto scat = gbits ? cs_scatter<8, true> : cs_scatter<8, false>;
+#endif
     cudaFuncSetAttribute(scat, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     scat<<<(unsigned)(nchunks_max * nslice), 256, smem, st>>>(
         (const uint32_t*)tka, (const uint32_t*)tva, (const uint32_t*)meta, n_views, (uint32_t)tpv, dbits, tslice,
