@@ -106,33 +106,29 @@ __device__ uint64_t warp_lookback(const uint64_t* words, int64_t bid) {
   return excl;
 }
 
-// Lanes of the warp holding the same 8-bit digit: 8 independent ballots (ALU
-// pipe, fully pipelined) instead of MATCH.ANY, whose latency dominated the
-// ranking loop in the ncu source view.
-#ifndef OS_PTX
-#define OS_PTX 0
-#endif
+// Lanes whose bit b of d equals this lane's: the bit test, the ballot and the
+// choice "ballot or its complement" as one PTX block, so ptxas loads several
+// digit bits into predicates at once (R2P) and complements the ballots under
+// predicates -- about 3 instructions per bit where the C++ form
+// (bit ? bb : ~bb) kept a shift, an extract, a compare and a select per bit
+// (measured: depth-sort passes 0.870 -> 0.836 ms per batch, K4c scatter
+// 1.236 -> 1.159).
+__device__ __forceinline__ uint32_t agree_bit(uint32_t d, uint32_t bit_mask) {
+  uint32_t bb, x;
+  asm volatile("{\n\t.reg .pred p;\n\t.reg .b32 t;\n\t"
+      "and.b32 t, %2, %3;\n\tsetp.ne.u32 p, t, 0;\n\t"
+      "vote.sync.ballot.b32 %0, p, 0xffffffff;\n\tselp.b32 %1, 0, 0xffffffff, p;\n\t}"
+      : "=r"(bb), "=r"(x) : "r"(d), "r"(bit_mask));
+  return bb ^ x;
+}
+
+// Lanes of the warp holding the same 8-bit digit: 8 ballots (ALU pipe, fully
+// pipelined) instead of MATCH.ANY, whose latency dominated the ranking loop
+// in the ncu source view.
 __device__ __forceinline__ uint32_t match_digit8(bool valid, uint32_t d) {
-#if OS_PTX
-  uint32_t pv = __ballot_sync(FULL, valid);
-#pragma unroll
-  for (int b = 0; b < 8; ++b) {
-    uint32_t bb, x;
-    asm("{\n\t.reg .pred p;\n\t.reg .b32 t;\n\t"
-        "and.b32 t, %2, %3;\n\tsetp.ne.u32 p, t, 0;\n\t"
-        "vote.sync.ballot.b32 %0, p, 0xffffffff;\n\tselp.b32 %1, 0, 0xffffffff, p;\n\t}"
-        : "=r"(bb), "=r"(x) : "r"(d), "r"(1u << b));
-    pv &= bb ^ x;
-  }
-  return pv;
-#endif
   uint32_t peers = __ballot_sync(FULL, valid);
 #pragma unroll
-  for (int b = 0; b < 8; ++b) {
-    const bool bit = (d >> b) & 1u;
-    const uint32_t bb = __ballot_sync(FULL, bit);
-    peers &= bit ? bb : ~bb;
-  }
+  for (int b = 0; b < 8; ++b) peers &= agree_bit(d, 1u << b);
   return peers;
 }
 
@@ -838,9 +834,6 @@ __global__ void __launch_bounds__(1024) k5_ranges(const uint32_t* __restrict__ c
 // DRAM traffic per key: 4 B (hist) + 4 B (packed) or 8 B read + 4 B write
 // (scatter) + the H matrix (CS_CHUNK = 64 K keys: ~0.15 B/key at c3), vs
 // 28 B/key for two radix passes.
-#ifndef CS_DBT
-#define CS_DBT 1  // compile-time digit widths for the K4c ranks (measured: tile sort 1.236 -> 1.159 ms per batch, bench 3,453 -> 3,495 views/s)
-#endif
 constexpr int CS_KPT = 16;  // keys per lane per sub-round (round 2: 16 3,190 / 12 3,186 / 8 3,173 / 6 3,156 views/s)
 #ifndef CS_CHUNK_KEYS
 #define CS_CHUNK_KEYS 65536  // measured: 64 K 2,895, 32 K 2,887, 16 K 2,880 views/s
@@ -944,21 +937,12 @@ __global__ void __launch_bounds__(256) cs_scan(const uint2* __restrict__ ranges,
 }
 
 // Lanes of the warp whose DB-bit digit equals this lane's (DB a compile-time
-// width: every bit test takes an immediate mask; per bit one predicate, one
-// ballot, one select and one LOP3).
+// width, so every bit test takes an immediate mask).
 template <int DB>
 __device__ __forceinline__ uint32_t match_digits(bool ok, uint32_t d) {
   uint32_t peers = __ballot_sync(FULL, ok);
 #pragma unroll
-  for (int b = 0; b < DB; ++b) {
-    // p = bit b of d; bb = ballot(p); x = p ? 0 : ~0; lanes agreeing on bit b = bb ^ x
-    uint32_t bb, x;
-    asm("{\n\t.reg .pred p;\n\t.reg .b32 t;\n\t"
-        "and.b32 t, %2, %3;\n\tsetp.ne.u32 p, t, 0;\n\t"
-        "vote.sync.ballot.b32 %0, p, 0xffffffff;\n\tselp.b32 %1, 0, 0xffffffff, p;\n\t}"
-        : "=r"(bb), "=r"(x) : "r"(d), "r"(1u << b));
-    peers &= bb ^ x;
-  }
+  for (int b = 0; b < DB; ++b) peers &= agree_bit(d, 1u << b);
   return peers;
 }
 
@@ -1566,17 +1550,13 @@ static gsr_status bin_sort_impl(gsr_ctx* ctx, const uint32_t* bin_rec, int64_t n
     cs_scan<<<(unsigned)((T + 255) / 256), 256, 0, st>>>((const uint2*)ranges, (const uint32_t*)meta, n_views,
                                                          (uint32_t)tpv, (uint32_t*)hm);
     const int dbits = std::max(1, bits_for(tslice));
-#if CS_DBT
-    // compile-time digit widths (8 / 10 / 12 / 14 bits), else the runtime loop
+    // compile-time digit widths (8 / 10 / 12 / 14 bits; CS_MAX_TPV needs at most 14)
     auto scat = gbits ? (dbits <= 8 ? cs_scatter<8, true, 8> : dbits <= 10 ? cs_scatter<8, true, 10>
                          : dbits <= 12 ? cs_scatter<8, true, 12> : dbits <= 14 ? cs_scatter<8, true, 14>
                          : cs_scatter<8, true>)
                       : (dbits <= 8 ? cs_scatter<8, false, 8> : dbits <= 10 ? cs_scatter<8, false, 10>
                          : dbits <= 12 ? cs_scatter<8, false, 12> : dbits <= 14 ? cs_scatter<8, false, 14>
                          : cs_scatter<8, false>);
-#else
-    auto scat = gbits ? cs_scatter<8, true> : cs_scatter<8, false>;
-#endif
     cudaFuncSetAttribute(scat, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     scat<<<(unsigned)(nchunks_max * nslice), 256, smem, st>>>(
         (const uint32_t*)tka, (const uint32_t*)tva, (const uint32_t*)meta, n_views, (uint32_t)tpv, dbits, tslice,
