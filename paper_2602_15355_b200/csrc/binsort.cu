@@ -834,6 +834,12 @@ __global__ void __launch_bounds__(1024) k5_ranges(const uint32_t* __restrict__ c
 // DRAM traffic per key: 4 B (hist) + 4 B (packed) or 8 B read + 4 B write
 // (scatter) + the H matrix (CS_CHUNK = 64 K keys: ~0.15 B/key at c3), vs
 // 28 B/key for two radix passes.
+#ifndef CS_PF
+#define CS_PF 1  // packed words of the next sub-round loaded during this one's prefix / scatter
+#endif
+#ifndef CS_MINB
+#define CS_MINB 3
+#endif
 constexpr int CS_KPT = 16;  // keys per lane per sub-round (round 2: 16 3,190 / 12 3,186 / 8 3,173 / 6 3,156 views/s)
 #ifndef CS_CHUNK_KEYS
 #define CS_CHUNK_KEYS 65536  // measured: 64 K 2,895, 32 K 2,887, 16 K 2,880 views/s
@@ -947,7 +953,7 @@ __device__ __forceinline__ uint32_t match_digits(bool ok, uint32_t d) {
 }
 
 template <int W, bool PACK, int DB = 0>
-__global__ void __launch_bounds__(W * 32, 3) cs_scatter(const uint32_t* __restrict__ tkeys,
+__global__ void __launch_bounds__(W * 32, CS_MINB) cs_scatter(const uint32_t* __restrict__ tkeys,
                                                      const uint32_t* __restrict__ tvals,
                                                      const uint32_t* __restrict__ meta, int V, uint32_t tpv,
                                                      int dbits, uint32_t tslice, int nslice,
@@ -986,6 +992,7 @@ __global__ void __launch_bounds__(W * 32, 3) cs_scatter(const uint32_t* __restri
   constexpr uint32_t SUB = W * 32 * CS_KPT;
   // packed words of the next sub-round are loaded during this one's prefix
   // and scatter (measured +0.15 %; the two-plane layout loads in place)
+#if CS_PF
   uint32_t nw[CS_KPT];
   if (PACK) {
 #pragma unroll
@@ -994,6 +1001,7 @@ __global__ void __launch_bounds__(W * 32, 3) cs_scatter(const uint32_t* __restri
       nw[k] = i < k1 ? __ldg(tkeys + i) : 0xffffffffu;
     }
   }
+#endif
   for (uint32_t s0 = k0; s0 < k1; s0 += SUB) {
     const uint32_t wb = s0 + (uint32_t)warp * (32 * CS_KPT);
     uint32_t dg[CS_KPT], vv[CS_KPT], rk[CS_KPT];
@@ -1001,7 +1009,11 @@ __global__ void __launch_bounds__(W * 32, 3) cs_scatter(const uint32_t* __restri
     for (int k = 0; k < CS_KPT; ++k) {
       const uint32_t i = wb + k * 32 + lane;
       if (PACK) {
+#if CS_PF
         const uint32_t wd = nw[k];
+#else
+        const uint32_t wd = i < k1 ? __ldg(tkeys + i) : 0xffffffffu;
+#endif
         dg[k] = i < k1 ? (wd >> gbits) - tb : 0xffffffffu;  // out of the slice: >= tn
         vv[k] = wd & ((1u << gbits) - 1u);
       } else {
@@ -1031,6 +1043,7 @@ __global__ void __launch_bounds__(W * 32, 3) cs_scatter(const uint32_t* __restri
       __syncwarp();
       rk[k] = pre + __popc(peers & lt);
     }
+#if CS_PF
     if (PACK) {
 #pragma unroll
       for (int k = 0; k < CS_KPT; ++k) {
@@ -1038,6 +1051,7 @@ __global__ void __launch_bounds__(W * 32, 3) cs_scatter(const uint32_t* __restri
         nw[k] = i < k1 ? __ldg(tkeys + i) : 0xffffffffu;
       }
     }
+#endif
     __syncthreads();
     // exclusive prefix over the warps, four tiles per 64-bit word (no carry:
     // a sub-round holds at most W x 32 x CS_KPT < 2^16 keys); the bases of
