@@ -72,6 +72,23 @@ __device__ __forceinline__ T warp_incl_scan(T v) {
   return v;
 }
 
+#ifndef SCAN_PTX
+#define SCAN_PTX 1
+#endif
+#if SCAN_PTX
+// u32: the shuffle's own in-range predicate guards the add (2 instructions per
+// step instead of shuffle, select, add)
+template <>
+__device__ __forceinline__ uint32_t warp_incl_scan<uint32_t>(uint32_t v) {
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1)
+    asm volatile("{\n\t.reg .pred p;\n\t.reg .b32 t;\n\t"
+                 "shfl.sync.up.b32 t|p, %0, %1, 0, 0xffffffff;\n\t@p add.u32 %0, %0, t;\n\t}"
+                 : "+r"(v) : "r"(o));
+  return v;
+}
+#endif
+
 template <typename T>
 __device__ __forceinline__ T warp_sum(T v) {
 #pragma unroll
@@ -492,7 +509,13 @@ __global__ void __launch_bounds__(256, (KPT <= 8 ? 4 : OS_MINB12)) onesweep(cons
 // the remaining widths).  Keys leave in
 // unit order, i.e. (depth, g, ty, tx) order, contiguously from the block's
 // look-back offset.
-constexpr int K3_ROUNDS = 4;
+#ifndef K3_ROUNDS_N
+#define K3_ROUNDS_N 4
+#endif
+constexpr int K3_ROUNDS = K3_ROUNDS_N;
+#ifndef K3_OWNER_OR
+#define K3_OWNER_OR 1
+#endif
 #ifndef K3_LS
 #define K3_LS 8  // keys per row written lane-serially (0: every key dealt 32 at a time; measured 0 / 3 / 4 / 6 / 8 / 12: emit 1.049 / 1.050 / 1.053 / 0.977 / 0.971 / 0.992 ms per batch, bench 3,401 / 3,405 / 3,423 / 3,453 / 3,456 / 3,447 views/s)
 #endif
@@ -588,9 +611,23 @@ __global__ void __launch_bounds__(256, K3_MINB) k3_emit(const KeyT* __restrict__
     const uint32_t rinc = warp_incl_scan<uint32_t>(nrows);
     const uint32_t rexcl = rinc - nrows;
     const uint32_t rtot = __shfl_sync(FULL, rinc, 31);
+#if K3_OWNER_OR
+    // every entry of a round has >= 1 tile row (entries past nvis, all at the
+    // end, have none), so the owner of slot j is the number of entries whose
+    // first row is at or before j, minus one: one OR-reduction of the step's
+    // row-start bits and a popcount instead of a 5-step shuffle search
+    int s_carry = -1;
+#endif
     for (uint32_t ub = 0; ub < rtot; ub += 32) {
       const uint32_t j = ub + lane;
+#if K3_OWNER_OR
+      const uint32_t dd = rexcl - ub;  // < 32: this entry's first row is in this step
+      const uint32_t M = __reduce_or_sync(FULL, (dd < 32u && nrows) ? (1u << dd) : 0u);
+      const int s = s_carry + __popc(M & (0xffffffffu >> (31 - lane)));
+      s_carry = __shfl_sync(FULL, s, 31);
+#else
       const int s = owner_of(rexcl, j);
+#endif
       const float u = __uint_as_float(__shfl_sync(FULL, s0[r].x, s));
       const float v = __uint_as_float(__shfl_sync(FULL, s0[r].y, s));
       const float sp = __uint_as_float(__shfl_sync(FULL, s0[r].z, s));
