@@ -516,6 +516,9 @@ constexpr int K3_ROUNDS = K3_ROUNDS_N;
 #ifndef K3_OWNER_OR
 #define K3_OWNER_OR 1
 #endif
+#ifndef K3_GENERIC_CNT
+#define K3_GENERIC_CNT 1
+#endif
 #ifndef K3_LS
 #define K3_LS 8  // keys per row written lane-serially (0: every key dealt 32 at a time; measured 0 / 3 / 4 / 6 / 8 / 12: emit 1.049 / 1.050 / 1.053 / 0.977 / 0.971 / 0.992 ms per batch, bench 3,401 / 3,405 / 3,423 / 3,453 / 3,456 / 3,447 views/s)
 #endif
@@ -652,26 +655,38 @@ __global__ void __launch_bounds__(256, K3_MINB) k3_emit(const KeyT* __restrict__
       const uint32_t wexcl = winc - w;
       const uint32_t wt = __shfl_sync(FULL, winc, 31);
 #if K3_LS > 0
+      // key slots in 32-bit arithmetic (K < 2^32, as the tile sort's u32
+      // positions already require): one wide multiply-add per address
+      const uint32_t b32 = (uint32_t)base;
       // each lane writes the first K3_LS keys of its own row span (the same
-      // slots the dealt loop would use: base + wexcl + i); only the keys of
+      // slots the dealt loop would use: b32 + wexcl + i); only the keys of
       // rows wider than K3_LS tiles go through the dealt loop below
       const uint32_t wmax = __reduce_max_sync(FULL, w);
+#if K3_GENERIC_CNT
+      // a row span lies in one view: its counters are all in the block's
+      // shared histogram or all global -- one generic pointer per row
+      uint32_t* cp = (kb - lo < (uint32_t)smem_bins) ? s_cnt + (kb - lo) : counts + kb;
+#endif
 #pragma unroll
       for (uint32_t i = 0; i < (uint32_t)K3_LS; ++i) {
         if (i >= wmax) break;
         if (i < w) {
           const uint32_t key = kb + i;
-          GSR_DCHECK(base + wexcl + i < kcap && key < T);
+          GSR_DCHECK(b32 + wexcl + i < kcap && key < T);
           if (PACK) {
-            tkeys[base + wexcl + i] = kl + (i << gbits);
+            tkeys[b32 + wexcl + i] = kl + (i << gbits);
           } else {
-            tkeys[base + wexcl + i] = key;
-            tvals[base + wexcl + i] = kl;
+            tkeys[b32 + wexcl + i] = key;
+            tvals[b32 + wexcl + i] = kl;
           }
+#if K3_GENERIC_CNT
+          atomicAdd(cp + i, 1u);
+#else
           if (key - lo < (uint32_t)smem_bins)
             atomicAdd(s_cnt + (key - lo), 1u);
           else
             atomicAdd(counts + key, 1u);
+#endif
         }
       }
       if (wmax > (uint32_t)K3_LS) {
@@ -689,12 +704,12 @@ __global__ void __launch_bounds__(256, K3_MINB) k3_emit(const KeyT* __restrict__
           if (k < w2t) {
             const uint32_t i = (uint32_t)K3_LS + (k - ow2);
             const uint32_t key = okb + i;
-            GSR_DCHECK(base + owx + i < kcap && key < T);
+            GSR_DCHECK(b32 + owx + i < kcap && key < T);
             if (PACK) {
-              tkeys[base + owx + i] = okl + (i << gbits);
+              tkeys[b32 + owx + i] = okl + (i << gbits);
             } else {
-              tkeys[base + owx + i] = key;
-              tvals[base + owx + i] = okl;
+              tkeys[b32 + owx + i] = key;
+              tvals[b32 + owx + i] = okl;
             }
             if (key - lo < (uint32_t)smem_bins)
               atomicAdd(s_cnt + (key - lo), 1u);
