@@ -42,11 +42,11 @@ def parse():
     p.add_argument("--steps", type=int, default=5)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="gsr", choices=["gsr", "reference"])
-    p.add_argument("--batch-views", type=int, default=32)  # measured: 64 2,903 / 32 2,889 / 16 2,866 views/s
+    p.add_argument("--batch-views", type=int, default=32)  # r2k: 32 3,547 / 48 3,546 / 64 3,518 views/s
     p.add_argument("--slots", type=int, default=3,
-                   help="concurrent batch pipelines (stream pairs); measured 3: 3,090, 2: 3,076 views/s")
+                   help="concurrent batch pipelines (stream pairs); r2k: 3: 3,547, 2: 3,443, 4: 3,542 views/s")
     p.add_argument("--k6-residency", type=int, default=10,
-                   help="persistent K6 blocks per SM when batches overlap (gsr_set_composite_residency)")
+                   help="persistent K6 blocks per SM when batches overlap (gsr_set_composite_residency); r2k: 10: 3,547, 8: 3,535, 12: 3,512 views/s")
     p.add_argument("--cpu-views", type=int, default=0, help="oracle sample size (0 = auto)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
